@@ -1,0 +1,384 @@
+"""Benchmark: decoded+rendered 1080p frames/sec (BASELINE config 2).
+
+Workload: a synthetic 300k-Gaussian, 6-layer, 300-frame sequence (10 motion
+groups, SH degree 1; SURVEY 8(d) recipe, seed 1002 + rank) encoded with the
+reference's bitstream; camera looking_at(eye=(0,0,-2.5)), 60 deg, 1920x1080.
+One step = decode layers 1..k of the whole container (range decode + CRC of
+every run, as decode_video does) and render every frame at 1080p.  The
+headline is k = 6 with the reference's default codec (1, range coded); the
+per-layer sweep k = 1..6 for both codecs is reported alongside.
+
+value: container bytes already resident in HBM (gsv_video_open_resident),
+       CUDA events on the session stream, max over ranks.
+e2e:   the C-ABI call with HOST buffers (gsv_video_open on host bytes, which
+       stages the layer-prefix payload H2D) + a D2H of every rendered frame as
+       u8 RGB into pinned memory, all inside the timed region.
+Multi-GPU: one process per GPU, each rank decodes+renders its own sequence
+(no data-path collective; weak scaling); a gloo/NCCL all_reduce(max) of the
+times after the barrier.
+
+--impl reference: times the CPU oracle (oracle/, the restatement of the
+reference's decode_video + render_set; the reference package itself is
+pure Python and cannot travel to the GPU box) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded+rendered 1080p frames/sec (layers L1-L6; ms/frame; HBM roofline %)"
+CACHE = Path(os.environ.get("GSV_BENCH_CACHE", "/tmp/gsv_bench_cache"))
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--gaussians", type=int, default=300_000)
+    p.add_argument("--layers", type=int, default=6)
+    p.add_argument("--frames", type=int, default=300)
+    p.add_argument("--group", type=int, default=30)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--k", type=int, default=6, help="layer prefix of the headline")
+    p.add_argument("--codec", type=int, default=1, choices=[0, 1])
+    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-sample-frames", type=int, default=2)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(a, seed):
+    """Container bytes for both codecs (cached on local disk by recipe)."""
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    key = hashlib.sha256(json.dumps([a.gaussians, a.layers, a.frames, a.group, seed, 3]).encode()
+                         ).hexdigest()[:16]
+    paths = {c: CACHE / f"{key}_c{c}.gsv" for c in (0, 1)}
+    if all(p.exists() for p in paths.values()):
+        return {c: p.read_bytes() for c, p in paths.items()}, key
+    spec = benchmark_spec(a.gaussians, a.frames, a.group)
+    cfg = EncodeConfig(layer_count=a.layers, prune_fraction=0.0, motion_threshold=0.0025)
+    t0 = time.time()
+    blobs = encode_stream(lambda: iter_frames(spec, seed), cfg, codecs=(0, 1),
+                          positions_source=lambda: iter_frames(spec, seed, positions_only=True))
+    print(f"[bench] encoded {a.frames} frames x {a.gaussians} in {time.time() - t0:.1f}s",
+          file=sys.stderr, flush=True)
+    CACHE.mkdir(parents=True, exist_ok=True)
+    for c, p in paths.items():
+        tmp = p.with_suffix(".tmp")
+        tmp.write_bytes(blobs[c])
+        os.replace(tmp, p)
+    return blobs, key
+
+
+def camera(a):
+    from paper_2509_17513_b200.types import Camera
+    return Camera.looking_at(eye=(0.0, 0.0, -2.5), target=(0.0, 0.0, 0.0), fov_deg=60.0,
+                             width=a.width, height=a.height, near=0.01)
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() in ("active", "0x1", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def run_b200(a, rank, world, dist):
+    import numpy as np
+    import torch
+
+    import paper_2509_17513_b200 as gsvb
+    from paper_2509_17513_b200 import _lib
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    blobs, key = make_inputs(a, 1002 + rank)
+    cam = camera(a)
+    cs = _lib.camera_struct(cam)
+    sess = gsvb.Session(dev)
+    s = sess.stream
+    resident = {}
+    for c, b in blobs.items():
+        t = torch.empty(len(b) + 64, dtype=torch.uint8, device="cuda")
+        t[:len(b)].copy_(torch.frombuffer(bytearray(b), dtype=torch.uint8))
+        resident[c] = t
+    torch.cuda.synchronize()
+    ring = [torch.empty((a.height, a.width, 3), dtype=torch.float32, device="cuda")
+            for _ in range(4)]
+
+    def step_resident(codec, k):
+        v = gsvb.DeviceVideo(blobs[codec], k, session=sess, resident=resident[codec])
+        for t in range(v.frame_count):
+            v.render_async(t, cs, ring[t % len(ring)])
+        return v
+
+    # size the key buffers and check parity of counters once (stats path)
+    for codec in (0, 1):
+        v = gsvb.DeviceVideo(blobs[codec], a.layers, session=sess, resident=resident[codec])
+        _, st0 = v.render(0, cam, stats=True)
+        v.close()
+
+    def timed(codec, k, steps, warmup, e2e=False):
+        pinned = None
+        if e2e:
+            pinned = torch.empty((a.frames, a.height, a.width, 3), dtype=torch.uint8).pin_memory()
+            u8 = [torch.empty((a.height, a.width, 3), dtype=torch.uint8, device="cuda")
+                  for _ in range(4)]
+            host = torch.frombuffer(bytearray(blobs[codec]), dtype=torch.uint8).pin_memory()
+
+        def one():
+            if not e2e:
+                return step_resident(codec, k)
+            v = gsvb.DeviceVideo(host, k, session=sess)
+            for t in range(v.frame_count):
+                buf = u8[t % len(u8)]
+                v.render_async(t, cs, None, buf)
+                with torch.cuda.stream(s):
+                    pinned[t].copy_(buf, non_blocking=True)
+            return v
+
+        for _ in range(warmup):
+            one().close()
+        s.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = _lib.kernel_launches()
+        t_host0 = time.perf_counter()
+        e0.record(s)
+        for _ in range(steps):
+            one().close()
+        e1.record(s)
+        e1.synchronize()
+        t_host = time.perf_counter() - t_host0
+        launches = _lib.kernel_launches() - launches0
+        ms = e0.elapsed_time(e1)
+        # decode happens inside open(): its host-side part is inside the event
+        # window because the events bracket every call on the same stream
+        ms = max(ms, t_host * 1e3)
+        torch.cuda.synchronize()
+        if dist:
+            tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        frames = steps * a.frames * world
+        return frames / (ms / 1e3), ms / steps, launches
+
+    with Clocks(dev) as clk:
+        fps, ms_step, launches = timed(a.codec, a.k, a.steps, a.warmup)
+    clocks = clk.summary()
+
+    # stage profile of one step (separate pass: events perturb timing slightly)
+    _lib.profile_enable(True)
+    v = step_resident(a.codec, a.k)
+    s.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    v.close()
+
+    sweep = {}
+    if not a.no_sweep:
+        for codec in (0, 1):
+            sweep[f"codec{codec}"] = {}
+            for k in range(1, a.layers + 1):
+                f, m, _ = timed(codec, k, max(1, a.steps // 2), 1)
+                sweep[f"codec{codec}"][str(k)] = {"fps": round(f, 1),
+                                                  "ms_per_frame": round(1e3 / f * world, 4)}
+    e2e = None
+    if not a.no_e2e:
+        f, m, _ = timed(a.codec, a.k, max(1, a.steps // 2), 1, e2e=True)
+        info = gsvb.read_structure(blobs[a.codec])
+        h2d = 0
+        for g in info.groups:
+            offs = [e.offset for l in range(a.k) for e in g.channels[l]]
+            ends = [e.offset + e.size for l in range(a.k) for e in g.channels[l]]
+            h2d += max(ends) - min(offs)
+        e2e = {"value": round(f, 2), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(a.frames * a.width * a.height * 3)}
+
+    # roofline of the dominant stage
+    stage_ms = {k: v["ms"] for k, v in prof.items()}
+    dom = max(stage_ms, key=stage_ms.get)
+    roof = roofline(a, blobs[a.codec], dom, prof, st0)
+    result = {
+        "metric": METRIC, "value": round(fps, 2), "unit": "frames/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 3),
+        "ms_per_frame": round(ms_step / a.frames, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic (SURVEY 8(d) recipe, reference bitstream, seed 1002+rank)",
+        "config": {"workload": "config2: 300k Gaussians, 6 layers, 300 frames (10 groups), "
+                               "1080p, single camera",
+                   "gaussians": a.gaussians, "layers": a.layers, "frames": a.frames,
+                   "groups": a.frames // a.group, "resolution": [a.width, a.height],
+                   "k": a.k, "codec": a.codec, "parallelism": f"frame-sharded x{world}",
+                   "l2": f"inputs larger than L2 ({len(blobs[a.codec]) / 1e6:.0f} MB container)"},
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "roofline": roof, "stages_ms_per_frame": {k: round(v["ms"] / a.frames, 5)
+                                                  for k, v in prof.items()},
+        "render_stats": st0, "per_layer": sweep,
+    }
+    return result
+
+
+def stage_bytes(a, blob, stage, st):
+    """Algorithmic bytes of one step for a stage."""
+    n, nvis, K = st["n_splats"], st["n_visible"], st["n_keys"]
+    npx = a.width * a.height
+    per_frame = {
+        "project": 26 * n + 8 * n + 4 * n + 48 * nvis,        # codes in, key+idx+record out
+        "depth_sort": 7 * (2 * 12 * n),                          # 7 passes, read+write key+idx
+        "key_emit": 48 * 2 * nvis + 8 * nvis + 8 * K,           # gather records, counts, keys out
+        "tile_sort": 2 * (2 * 8 * K),                            # 2 passes, read+write key+val
+        "tile_ranges": 4 * K,
+        "composite": 4 * K + 48 * K + 12 * npx,                  # ranks, records, image
+    }
+    if stage in per_frame:
+        return per_frame[stage] * a.frames
+    return len(blob)  # decode stages: the container bytes read once per step
+
+
+def roofline(a, blob, stage, prof, st):
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    ms = prof[stage]["ms"]
+    b = stage_bytes(a, blob, stage, st)
+    achieved = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    return {"bound": "hbm", "kernel": stage, "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "algorithmic_bytes_per_step": int(b), "ms_per_step": round(ms, 3)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(a, threads, samples, rank_seed=1002):
+    """Oracle (CPU restatement) on a bounded sample: decode group 0 (all its
+    frames, layers <= k) + render `samples` frames, `threads` host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    blobs, _ = make_inputs(a, rank_seed)
+    data = blobs[a.codec]
+    cam = camera(a)
+    info = O.read_structure(data)
+    t0 = time.perf_counter()
+    vals = O.decode_group_codes(data, info, 0, a.k)
+    frames = O.assemble(info, info.groups[0], vals, a.k)
+    t_dec = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(lambda g: O.render_set(g, cam), frames[:samples]))
+    t_ren = time.perf_counter() - t0
+    gframes = info.groups[0].frame_count
+    per_frame = t_dec / gframes + t_ren / samples
+    return 1.0 / per_frame, {"decode_group_s": t_dec, "render_s": t_ren,
+                             "sample": f"group 0 range/raw decode of {gframes} frames at k={a.k} "
+                                       f"(amortised) + render of {samples} frames at "
+                                       f"{a.width}x{a.height}, {threads} threads"}
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        backend = "nccl" if a.impl == "b200" and torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        td.init_process_group(backend=backend)
+        dist = td
+    if a.impl == "reference":
+        if rank == 0:
+            threads = len(os.sched_getaffinity(0))
+            samples = max(a.cpu_sample_frames, min(threads, 8))
+            fps, det = cpu_reference(a, threads, samples)
+            line = {"metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+                    "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+                    "ms_per_step": round(1e3 / fps, 2), "higher_is_better": True,
+                    "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+                    "data": "synthetic (same recipe as the b200 arm)", "impl": "reference",
+                    "config": {"workload": "config2: 300k Gaussians, 6 layers, 300 frames, 1080p",
+                               "k": a.k, "codec": a.codec},
+                    "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": threads,
+                                     "kind": "port", "sample": det["sample"]},
+                    "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
+    res = run_b200(a, rank, world, dist)
+    if rank == 0:
+        if not a.no_cpu:
+            fps, det = cpu_reference(a, 1, a.cpu_sample_frames)
+            res["cpu_baseline"] = {"value": round(fps, 4), "unit": "frames/s", "cores": 1,
+                                   "kind": "port", "sample": det["sample"]}
+        print(json.dumps(res), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

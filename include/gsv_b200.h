@@ -1,0 +1,191 @@
+/*
+ * gsv_b200.h -- C ABI of libgsv_b200.so, the B200-native decode-and-render
+ * path of the `gsv` (4DGCPro) reference package.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  Every entry point
+ * replaces one reference interface; paths are relative to
+ * /root/reference/pkg/src/gsv/.  The reference is pure Python, so the
+ * reference-side binding is a ctypes stub; the package
+ * paper_2509_17513_b200 is exactly that stub plus the reference's
+ * dataclasses.
+ *
+ * Errors: every int-returning call returns GSV_OK or one of GSV_E_*; the
+ * matching message (the reference's exception text, e.g.
+ * "group 0 layer 3 channel sh[4]: checksum mismatch (corrupt or truncated
+ * payload)") is available from gsv_last_error() on the calling thread.
+ * GSV_E_INVALID_INPUT / FORMAT / CODEC map to the reference's
+ * InvalidInputError / FormatError / CodecError (errors.py:8-17).
+ *
+ * Pointers documented as "device" are CUDA device addresses on the
+ * session's device; "host" pointers are ordinary (ideally pinned) memory.
+ * All device work is issued on the session stream; calls that return host
+ * data synchronise that stream.
+ */
+#ifndef GSV_B200_H
+#define GSV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSV_ABI_VERSION 1
+
+enum {
+    GSV_OK = 0,
+    GSV_E_INVALID_INPUT = 1, /* errors.InvalidInputError */
+    GSV_E_FORMAT = 2,        /* errors.FormatError */
+    GSV_E_CODEC = 3,         /* errors.CodecError */
+    GSV_E_CUDA = 4,          /* CUDA runtime failure (no reference counterpart) */
+    GSV_E_NOMEM = 5
+};
+
+typedef struct gsv_session gsv_session; /* one CUDA device + stream + scratch */
+typedef struct gsv_video gsv_video;     /* a decoded layer prefix, resident in HBM */
+
+/* Camera (render.py:43-120): x_cam = R x_world + t, pinhole fx fy cx cy. */
+typedef struct gsv_camera {
+    double rotation[9]; /* row-major world-to-camera */
+    double translation[3];
+    double fx, fy, cx, cy;
+    double near_plane;
+    double background[3];
+    int32_t width, height;
+} gsv_camera;
+
+/* Header of a container (container.py:73-81) */
+typedef struct gsv_info {
+    int32_t version, layer_count, sh_degree, group_count;
+    int32_t fps_num, fps_den;
+    uint32_t flags;
+    float bounds[6];
+    uint64_t header_bytes; /* header + directory size */
+} gsv_info;
+
+typedef struct gsv_group_info { /* container.py:54-70 */
+    uint32_t start_frame;
+    uint32_t frame_count;
+    uint32_t position_bits;
+    uint32_t layer_counts[64];    /* first layer_count entries valid */
+    uint32_t channel_counts[64];  /* entries per layer */
+} gsv_group_info;
+
+typedef struct gsv_entry_info { /* container.py:44-51 */
+    int32_t attribute; /* quantize.py:23-30 codes */
+    int32_t component;
+    int32_t bits;
+    uint64_t offset, size;
+    float range_min, range_max;
+} gsv_entry_info;
+
+/* Per-render statistics (exposed for tests and the roofline accounting). */
+typedef struct gsv_render_stats {
+    int64_t n_splats;   /* splats projected (layer prefix size) */
+    int64_t n_visible;  /* survivors of project_set's culls */
+    int64_t n_keys;     /* (tile, rank) keys emitted */
+    int32_t tiles_x, tiles_y;
+} gsv_render_stats;
+
+const char* gsv_last_error(void);
+int gsv_last_error_kind(void);
+int gsv_abi_version(void);
+
+/* ---- sessions ---------------------------------------------------------- */
+/* stream: a cudaStream_t (0 = the session creates its own non-blocking stream). */
+int gsv_session_create(int device, uintptr_t stream, gsv_session** out);
+void gsv_session_destroy(gsv_session* s);
+/* Block until all work issued on the session stream has finished. */
+int gsv_session_sync(gsv_session* s);
+
+/* ---- container structure (read_structure / read_container_info,
+ *      container.py:151-196); host only ------------------------------------ */
+int gsv_read_info(const uint8_t* data, size_t len, gsv_info* out);
+int gsv_read_group(const uint8_t* data, size_t len, int group, gsv_group_info* out);
+int gsv_read_entry(const uint8_t* data, size_t len, int group, int layer, int entry,
+                   gsv_entry_info* out);
+
+/* ---- decode (read_layers / decode_video, container.py:260-310,
+ *      pipeline.py:350-359) --------------------------------------------------
+ * gsv_video_open: host container bytes; stages the layer-prefix payload
+ * bytes of every group into HBM (only layers <= up_to_layer are copied,
+ * mirroring the reference's prefix reads), range-decodes and CRC-checks
+ * every run on the GPU and validates the result in the reference's error
+ * order.  up_to_layer == -1 means all layers (decode_video's None).
+ * gsv_video_open_resident: same, but `dev_data` already holds the whole
+ * container in HBM (only `data` is read on the host, for the directory);
+ * the device allocation must extend at least 64 bytes past the container
+ * (the decoders read whole 16-byte chunks). */
+int gsv_video_open(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer,
+                   gsv_video** out);
+int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len,
+                            const uint8_t* dev_data, int up_to_layer, gsv_video** out);
+void gsv_video_close(gsv_video* v);
+int gsv_video_frame_count(const gsv_video* v);
+int gsv_video_decoded_layers(const gsv_video* v);
+/* DecodedVideo.frame(t) (container.py:219-223): group index of frame t, or -1 */
+int gsv_video_group_of(const gsv_video* v, int t);
+/* number of splats of every frame of group g at this layer prefix */
+int64_t gsv_video_group_splats(const gsv_video* v, int g);
+/* fp64 SoA of frame t (device outputs): pos (n,3) rot (n,4) scl (n,3) opac (n) sh (n,shdim) */
+int gsv_video_frame_values(gsv_video* v, int t, double* pos, double* rot, double* scl,
+                           double* opac, double* sh);
+/* decoded integer samples of frame t, (layer, slot) order, u32 (device), for parity tests:
+ * out[(layer_base + j) * nslots + slot] for splat j of that layer. */
+int gsv_video_frame_codes(gsv_video* v, int t, uint32_t* out);
+
+/* ---- render (render_set / render_progressive, render.py:382-398) --------
+ * Output: fp32 RGB (height, width, 3) in [0,1] (device), optional u8 RGB
+ * rounded like write_ppm (render.py:165-169).  Either output may be NULL. */
+int gsv_video_render(gsv_video* v, int t, const gsv_camera* cam, float* out_rgb,
+                     uint8_t* out_rgb8, gsv_render_stats* stats);
+/* render an fp64 SoA Gaussian set resident in HBM (render_set) */
+int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos,
+                   const double* rot, const double* scl, const double* opac, const double* sh,
+                   const gsv_camera* cam, float* out_rgb, uint8_t* out_rgb8,
+                   gsv_render_stats* stats);
+/* reconstruct_frame's fold (motion.py:165-235), in place on device SoA arrays:
+ * for each of nd deltas (device pointer tables on the host side):
+ *   q <- normalize(dq * q); p += dt; s <- max(s + ds, 1e-7);
+ *   o <- clip(o + do, 0, 1); sh += dsh
+ * Delta rows beyond n are ignored (FrameDelta.prefix). */
+int gsv_fold_deltas(gsv_session* s, int64_t n, int shdim, double* pos, double* rot,
+                    double* scl, double* opac, double* sh, int nd,
+                    const double* const* d_trans, const double* const* d_rot,
+                    const double* const* d_scl, const double* const* d_opac,
+                    const double* const* d_sh);
+/* projection outputs for parity tests (device): for every splat i,
+ * rect[i] = (x0,x1,y0,y1) or all zero when culled, depth[i], order[r] = i of
+ * depth-rank r (visible splats first, stable), tile_count[i]. */
+int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* pos,
+                      const double* rot, const double* scl, const double* opac,
+                      const double* sh, const gsv_camera* cam, int32_t* rects, double* depth,
+                      int32_t* order, int32_t* tile_count, int64_t* n_visible);
+
+/* ---- codec (decode_planes, codec.py:226-263): one payload, host buffers --
+ * hdr receives codec, bits, width, height, count; samples (count*h*w) as u32. */
+int gsv_decode_payload_host(gsv_session* s, const uint8_t* blob, size_t len,
+                            uint32_t* samples, size_t capacity, int32_t* hdr);
+
+/* ---- instrumentation ------------------------------------------------------
+ * gsv_kernel_launches: kernels launched by this library so far (process-wide).
+ * gsv_profile_enable(1) resets and starts stage timing with CUDA events on the
+ * launching streams; gsv_profile_read fills per-stage total ms and interval
+ * counts for stages 0..7 = project, depth sort, key emission, tile sort,
+ * tile ranges, composite, range decode, CRC. */
+long long gsv_kernel_launches(void);
+int gsv_profile_enable(int enable);
+int gsv_profile_read(double* ms, long long* intervals, int max_stages);
+
+/* ---- synthetic input tooling (encoder side; not on the decode path) ------
+ * Range-code one run of planes like codec.py:105-180 (codec 1) into `out`
+ * (payload body, without the 14-B header / CRC).  Returns body length or <0. */
+int64_t gsv_encode_reference_body(const uint32_t* samples, int count, int h, int w, int bits,
+                                  uint8_t* out, size_t capacity);
+uint32_t gsv_crc32(const uint8_t* data, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSV_B200_H */

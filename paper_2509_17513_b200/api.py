@@ -1,0 +1,515 @@
+"""Public decode/render API, a drop-in for the reference's entry points.
+
+Mirrors (paths relative to /root/reference/pkg/src/gsv/):
+  decode_video(source, up_to_layer=None)        pipeline.py:350-359
+  read_layers(source, up_to_layer)              container.py:260-310
+  read_structure(f) / read_container_info(path) container.py:151-196
+  decode_planes(payload)                        codec.py:226-263
+  render_set(gset, cam)                         render.py:382-385
+  render_progressive(frame, k, deltas, t, cam)  render.py:388-398
+  reconstruct_frame(keyframe, deltas, t, k)     motion.py:218-235
+with the same argument meaning, return types and exceptions.  All compute
+runs in libgsv_b200.so on the GPU; torch only provides device memory and
+the stream.  `DeviceVideo` is the zero-copy fast path: a decoded layer
+prefix resident in HBM that renders frames into device tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import io
+import threading
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, camera_struct
+from .errors import CodecError, FormatError, InvalidInputError
+from .types import (ATTRIBUTE_NAMES, ChannelEntry, ChannelId, CodedPayload, ContainerInfo,
+                    DecodedGroup, DecodedVideo, GaussianSet, GroupDirectory, Image, Plane,
+                    sh_coeff_count)
+
+_LE = {8: np.dtype("<u1"), 16: np.dtype("<u2"), 32: np.dtype("<u4")}
+
+
+# ---------------------------------------------------------------------------
+# sessions
+# ---------------------------------------------------------------------------
+class Session:
+    """A CUDA device + stream + scratch workspace inside libgsv_b200."""
+
+    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2509_17513_b200 needs a CUDA device (B200); none is visible")
+        L = _lib.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        h = ctypes.c_void_p()
+        check(L.gsv_session_create(self.device, self.stream.cuda_stream, ctypes.byref(h)))
+        self.handle = h
+        self.lib = L
+
+    def sync(self):
+        check(self.lib.gsv_session_sync(self.handle))
+
+    def close(self):
+        if self.handle:
+            self.lib.gsv_session_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+_sessions = threading.local()
+
+
+def default_session() -> Session:
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    d = getattr(_sessions, "by_device", None)
+    if d is None:
+        d = _sessions.by_device = {}
+    if dev not in d:
+        d[dev] = Session(dev)
+    return d[dev]
+
+
+def _pre(s: Session) -> None:
+    """Session stream waits for torch's pending work (inputs are ready)."""
+    s.stream.wait_stream(torch.cuda.current_stream(s.device))
+
+
+def _post(s: Session) -> None:
+    """torch's stream waits for the session's work (outputs are ready)."""
+    torch.cuda.current_stream(s.device).wait_stream(s.stream)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+# container structure (host only)
+# ---------------------------------------------------------------------------
+def _read_all(source) -> bytes:
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return bytes(source)
+    if isinstance(source, (str, Path)):
+        return Path(source).read_bytes()
+    return source.read()
+
+
+def _structure_from_bytes(data: bytes) -> ContainerInfo:
+    L = _lib.load()
+    info = _lib.Info_t()
+    check(L.gsv_read_info(data, len(data), ctypes.byref(info)))
+    groups = []
+    for g in range(info.group_count):
+        gi = _lib.GroupInfo_t()
+        check(L.gsv_read_group(data, len(data), g, ctypes.byref(gi)))
+        layers = []
+        for l in range(info.layer_count):
+            ents = []
+            for e in range(gi.channel_counts[l]):
+                ei = _lib.EntryInfo_t()
+                check(L.gsv_read_entry(data, len(data), g, l, e, ctypes.byref(ei)))
+                ents.append(ChannelEntry(ChannelId(ATTRIBUTE_NAMES[ei.attribute], ei.component),
+                                         ei.bits, ei.offset, ei.size, float(ei.range_min),
+                                         float(ei.range_max)))
+            layers.append(tuple(ents))
+        groups.append(GroupDirectory(gi.start_frame, gi.frame_count, gi.position_bits,
+                                     tuple(gi.layer_counts[:info.layer_count]), tuple(layers)))
+    return ContainerInfo(info.version, info.layer_count, info.sh_degree,
+                         (info.fps_num, info.fps_den), tuple(float(b) for b in info.bounds),
+                         info.flags, tuple(groups))
+
+
+def _read_prefix(f, up_to_layer: int | None):
+    """Read header + directory, then only the payload bytes of layers <= k
+    (container.py:276-283): the returned buffer has zeros elsewhere, so no
+    byte of a higher layer is ever read from `f`."""
+    start = f.tell()
+    head = f.read(42)
+    if len(head) < 42:
+        raise FormatError("unexpected end of container (wanted 42 bytes)")
+    # grow the directory read until the C parser is satisfied
+    want = 4096
+    while True:
+        f.seek(start)
+        blob = f.read(want)
+        try:
+            info = _structure_from_bytes(blob)
+            break
+        except FormatError as e:
+            if "unexpected end" in str(e) and len(blob) == want:
+                want *= 4
+                continue
+            raise
+    k = info.layer_count if up_to_layer is None else up_to_layer
+    if not 1 <= k <= info.layer_count:
+        raise InvalidInputError(f"layer {up_to_layer} out of range 1..{info.layer_count}")
+    end = 0
+    for g in info.groups:
+        for l in range(k):
+            for e in g.channels[l]:
+                end = max(end, e.offset + e.size)
+    buf = bytearray(max(end, len(blob)))
+    buf[:len(blob)] = blob
+    for g in info.groups:
+        for l in range(k):
+            for e in g.channels[l]:
+                f.seek(start + e.offset)
+                chunk = f.read(e.size)
+                buf[e.offset:e.offset + len(chunk)] = chunk
+                if len(chunk) < e.size:
+                    del buf[e.offset + len(chunk):]
+                    return bytes(buf), info, k
+    return bytes(buf), info, k
+
+
+def read_structure(f) -> ContainerInfo:
+    """read_structure (container.py:151-191) for a binary file object or bytes."""
+    if isinstance(f, (bytes, bytearray, memoryview)):
+        return _structure_from_bytes(bytes(f))
+    start = f.tell()
+    want = 4096
+    while True:
+        f.seek(start)
+        blob = f.read(want)
+        try:
+            info = _structure_from_bytes(blob)
+        except FormatError as e:
+            if "unexpected end" in str(e) and len(blob) == want:
+                want *= 4
+                continue
+            raise
+        return info
+
+
+def read_container_info(path) -> ContainerInfo:
+    with open(path, "rb") as f:
+        return read_structure(f)
+
+
+# ---------------------------------------------------------------------------
+# decode
+# ---------------------------------------------------------------------------
+class DeviceVideo:
+    """A layer prefix of a container decoded into HBM (gsv_video_open).
+
+    Only the payload bytes of layers 1..k are staged; every range-coded run
+    is decoded and CRC-checked on the GPU before this returns, with the
+    reference's exceptions on failure.  Frames are then rendered (or
+    materialised) on demand straight from the decoded code planes.
+    """
+
+    def __init__(self, source, up_to_layer: int | None = None, session: Session | None = None,
+                 resident: torch.Tensor | None = None):
+        self.session = session or default_session()
+        L = self.session.lib
+        ptr = None
+        if isinstance(source, torch.Tensor):
+            # host (ideally pinned) uint8 tensor holding the whole container
+            if source.is_cuda or source.dtype != torch.uint8:
+                raise InvalidInputError("source tensor must be a host uint8 tensor")
+            src = source.contiguous()
+            ptr, n = src.data_ptr(), src.numel()
+            want = 1 << 16
+            while True:
+                head = bytes(src[:min(n, want)].numpy())
+                try:
+                    info = _structure_from_bytes(head)
+                    break
+                except FormatError as e:
+                    if "unexpected end" in str(e) and want < n:
+                        want *= 4
+                        continue
+                    raise
+            k = info.layer_count if up_to_layer is None else up_to_layer
+            data = src
+        elif isinstance(source, (str, Path)):
+            with open(source, "rb") as f:
+                data, info, k = _read_prefix(f, up_to_layer)
+        elif isinstance(source, (bytes, bytearray, memoryview)):
+            data = bytes(source)
+            info = _structure_from_bytes(data)
+            k = info.layer_count if up_to_layer is None else up_to_layer
+        else:
+            data, info, k = _read_prefix(source, up_to_layer)
+        if not 1 <= k <= info.layer_count:
+            raise InvalidInputError(f"layer {up_to_layer} out of range 1..{info.layer_count}")
+        self.info = info
+        self._data = data
+        h = ctypes.c_void_p()
+        _pre(self.session)
+        nbytes = data.numel() if ptr is not None else len(data)
+        hptr = ptr if ptr is not None else data
+        if resident is not None:
+            check(L.gsv_video_open_resident(self.session.handle, hptr, nbytes,
+                                            resident.data_ptr(), k, ctypes.byref(h)))
+        else:
+            check(L.gsv_video_open(self.session.handle, hptr, nbytes, k, ctypes.byref(h)))
+        self.handle = h
+        self.lib = L
+        self.decoded_layers = L.gsv_video_decoded_layers(h)
+        self.frame_count = L.gsv_video_frame_count(h)
+        self.sh_degree = info.sh_degree
+        self.shdim = sh_coeff_count(info.sh_degree)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.gsv_video_close(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def group_of(self, t: int) -> int:
+        """Group assignment of frame t (container.py:219-223); -1 if none."""
+        return self.lib.gsv_video_group_of(self.handle, int(t))
+
+    def splat_count(self, t: int) -> int:
+        g = self.group_of(t)
+        if g < 0:
+            raise InvalidInputError(f"frame {t} out of range 0..{self.frame_count - 1}")
+        return int(self.lib.gsv_video_group_splats(self.handle, g))
+
+    def frame_tensors(self, t: int) -> dict:
+        """fp64 SoA of frame t on the device (positions, rotations, ...)."""
+        n = self.splat_count(t)
+        dev = torch.device("cuda", self.session.device)
+        out = {"positions": torch.empty((n, 3), dtype=torch.float64, device=dev),
+               "rotations": torch.empty((n, 4), dtype=torch.float64, device=dev),
+               "scales": torch.empty((n, 3), dtype=torch.float64, device=dev),
+               "opacities": torch.empty((n,), dtype=torch.float64, device=dev),
+               "sh": torch.empty((n, self.shdim), dtype=torch.float64, device=dev)}
+        _pre(self.session)
+        check(self.lib.gsv_video_frame_values(self.handle, int(t), *(
+            _ptr(out[k]) for k in ("positions", "rotations", "scales", "opacities", "sh"))))
+        _post(self.session)
+        return out
+
+    def frame(self, t: int) -> GaussianSet:
+        """DecodedVideo.frame(t) materialised on the host (fp64)."""
+        d = self.frame_tensors(t)
+        self.session.sync()
+        return GaussianSet(*(d[k].cpu().numpy() for k in
+                             ("positions", "rotations", "scales", "opacities", "sh")),
+                           self.sh_degree)
+
+    def frame_codes(self, t: int) -> torch.Tensor:
+        """Decoded integer samples of frame t: (n, 11 + shdim) uint32 in slot
+        order position[0..2], rotation[0..3], scales[0..2], opacity, sh[..]."""
+        n = self.splat_count(t)
+        out = torch.empty((n, 11 + self.shdim), dtype=torch.int32,
+                          device=torch.device("cuda", self.session.device))
+        _pre(self.session)
+        check(self.lib.gsv_video_frame_codes(self.handle, int(t), _ptr(out)))
+        _post(self.session)
+        return out
+
+    def render(self, t: int, cam, out: torch.Tensor | None = None,
+               out_u8: torch.Tensor | None = None, stats: bool = False):
+        """Render frame t (render_set of DecodedVideo.frame(t)) into an fp32
+        (H, W, 3) device tensor; optionally also u8 (write_ppm rounding)."""
+        c = camera_struct(cam)
+        dev = torch.device("cuda", self.session.device)
+        if out is None and out_u8 is None:
+            out = torch.empty((c.height, c.width, 3), dtype=torch.float32, device=dev)
+        st = _lib.RenderStats_t()
+        _pre(self.session)
+        check(self.lib.gsv_video_render(self.handle, int(t), ctypes.byref(c), _ptr(out),
+                                        _ptr(out_u8), ctypes.byref(st)))
+        _post(self.session)
+        if stats:
+            return out, {"n_splats": st.n_splats, "n_visible": st.n_visible,
+                         "n_keys": st.n_keys, "tiles": (st.tiles_x, st.tiles_y)}
+        return out
+
+    def render_async(self, t: int, cam_struct, out: torch.Tensor | None,
+                     out_u8: torch.Tensor | None = None):
+        """Enqueue a render without synchronising (throughput mode).  The key
+        buffer must already be large enough (render one frame with
+        stats=True first); `check_overflow()` after a sync verifies it."""
+        check(self.lib.gsv_video_render(self.handle, int(t), ctypes.byref(cam_struct), _ptr(out),
+                                        _ptr(out_u8), ctypes.c_void_p(1)))
+
+    def to_decoded_video(self) -> DecodedVideo:
+        groups = []
+        k = self.decoded_layers
+        for g in self.info.groups:
+            frames = tuple(self.frame(g.start_frame + i) for i in range(g.frame_count))
+            groups.append(DecodedGroup(g.start_frame, g.frame_count, tuple(g.layer_counts[:k]),
+                                       frames))
+        return DecodedVideo(self.info.layer_count, k, self.info.sh_degree, self.info.fps,
+                            tuple(groups))
+
+
+def read_layers(source, up_to_layer: int) -> DecodedVideo:
+    """read_layers (container.py:260-310): decode layers 1..k of every group."""
+    with DeviceVideo(source, up_to_layer) as v:
+        return v.to_decoded_video()
+
+
+def decode_video(source, up_to_layer: int | None = None) -> DecodedVideo:
+    """decode_video (pipeline.py:350-359)."""
+    if up_to_layer is None:
+        if not isinstance(source, (str, Path, bytes, bytearray, memoryview)):
+            pos = source.tell()
+            up_to_layer = read_structure(source).layer_count
+            source.seek(pos)
+    return read_layers(source, up_to_layer)
+
+
+def decode_planes(payload) -> list:
+    """decode_planes (codec.py:226-263) on the GPU: list of Plane."""
+    blob = payload.to_bytes() if hasattr(payload, "to_bytes") else bytes(payload)
+    s = default_session()
+    n = max(1, int(payload.count) * int(payload.width) * int(payload.height))
+    out = np.zeros(n, np.uint32)
+    hdr = np.zeros(5, np.int32)
+    check(s.lib.gsv_decode_payload_host(s.handle, blob, len(blob), out.ctypes.data, out.size,
+                                        hdr.ctypes.data))
+    bits = int(payload.bits)
+    arr = out[:int(payload.count) * int(payload.width) * int(payload.height)].astype(_LE[bits])
+    arr = arr.reshape(int(payload.count), int(payload.height), int(payload.width))
+    planes = []
+    for i in range(arr.shape[0]):
+        s_ = arr[i].copy()
+        s_.flags.writeable = False
+        planes.append(Plane(samples=s_, valid_count=arr.shape[1] * arr.shape[2]))
+    return planes
+
+
+# ---------------------------------------------------------------------------
+# render
+# ---------------------------------------------------------------------------
+def _soa_to_device(gset, dev):
+    return [torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(gset, k), dtype=np.float64)))
+            .to(dev) for k in ("positions", "rotations", "scales", "opacities", "sh")]
+
+
+def render_soa_tensors(tensors, sh_degree: int, cam, session: Session | None = None,
+                       out: torch.Tensor | None = None, stats: bool = False):
+    """Render device fp64 SoA tensors; returns an fp32 (H, W, 3) device tensor."""
+    s = session or default_session()
+    c = camera_struct(cam)
+    n = int(tensors[0].shape[0])
+    if out is None:
+        out = torch.empty((c.height, c.width, 3), dtype=torch.float32,
+                          device=torch.device("cuda", s.device))
+    st = _lib.RenderStats_t()
+    _pre(s)
+    check(s.lib.gsv_render_soa(s.handle, n, int(sh_degree), *(_ptr(t) for t in tensors),
+                               ctypes.byref(c), _ptr(out), None, ctypes.byref(st)))
+    _post(s)
+    if stats:
+        return out, {"n_splats": st.n_splats, "n_visible": st.n_visible, "n_keys": st.n_keys,
+                     "tiles": (st.tiles_x, st.tiles_y)}
+    return out
+
+
+def render_set(gset, cam) -> Image:
+    """render_set (render.py:382-385)."""
+    s = default_session()
+    dev = torch.device("cuda", s.device)
+    img = render_soa_tensors(_soa_to_device(gset, dev), gset.sh_degree, cam, s)
+    return Image(pixels=img.cpu().numpy().astype(np.float64))
+
+
+def _fold_device(t_list, deltas, count, shdim, s: Session):
+    dev = torch.device("cuda", s.device)
+    keep = []
+    for d in deltas:
+        if len(d.rigid.translations) < count:
+            raise InvalidInputError("delta shorter than the requested layer prefix")
+        arrs = [torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)[:count]))
+                .to(dev) for a in (d.rigid.translations, d.rigid.rotations, d.residual.d_scales,
+                                   d.residual.d_opacity, d.residual.d_sh)]
+        if arrs[4].shape[1] != shdim:
+            raise InvalidInputError("d_sh width does not match the set's SH degree")
+        keep.append(arrs)
+    nd = len(keep)
+    if nd == 0 or count == 0:
+        return
+    P = ctypes.c_void_p * nd
+    tabs = [P(*[k[j].data_ptr() for k in keep]) for j in range(5)]
+    _pre(s)
+    check(s.lib.gsv_fold_deltas(s.handle, count, shdim, *(x.data_ptr() for x in t_list), nd,
+                                *[ctypes.cast(tb, ctypes.c_void_p) for tb in tabs]))
+    _post(s)
+
+
+def _flatten(keyframe, up_to_layer):
+    layers = keyframe.layers
+    k = len(layers) if up_to_layer is None else up_to_layer
+    if not 1 <= k <= len(layers):
+        raise InvalidInputError(f"layer index {k} out of range 1..{len(layers)}")
+    return layers[:k]
+
+
+def reconstruct_frame_tensors(group_keyframe, deltas: Sequence, t: int, up_to_layer=None,
+                              session: Session | None = None):
+    """reconstruct_frame on the device: returns (tensors, sh_degree)."""
+    s = session or default_session()
+    if not 0 <= t <= len(deltas):
+        raise InvalidInputError(f"frame index {t} out of range 0..{len(deltas)}")
+    layers = _flatten(group_keyframe, up_to_layer)
+    dev = torch.device("cuda", s.device)
+    parts = [_soa_to_device(l, dev) for l in layers]
+    tensors = [torch.cat([p[i] for p in parts]).contiguous() for i in range(5)]
+    deg = layers[0].sh_degree
+    _fold_device(tensors, list(deltas[:t]), int(tensors[0].shape[0]), sh_coeff_count(deg), s)
+    return tensors, deg
+
+
+def reconstruct_frame(group_keyframe, deltas: Sequence, t: int, up_to_layer=None) -> GaussianSet:
+    """reconstruct_frame (motion.py:218-235)."""
+    tensors, deg = reconstruct_frame_tensors(group_keyframe, deltas, t, up_to_layer)
+    return GaussianSet(*(x.cpu().numpy() for x in tensors), deg)
+
+
+def render_progressive(frame, up_to_layer: int, deltas, t: int, cam) -> Image:
+    """render_progressive (render.py:388-398)."""
+    if not 1 <= up_to_layer <= len(frame.layers):
+        raise InvalidInputError(f"layer {up_to_layer} out of range 1..{len(frame.layers)}")
+    tensors, deg = reconstruct_frame_tensors(frame, deltas, t, up_to_layer)
+    img = render_soa_tensors(tensors, deg, cam)
+    return Image(pixels=img.cpu().numpy().astype(np.float64))
+
+
+def project_debug(gset, cam, session: Session | None = None):
+    """Projection outputs for parity checks: rects (n,4; zeros when culled),
+    depth (n), order (depth-rank -> splat index, survivors first), tile
+    counts (n) and the survivor count."""
+    s = session or default_session()
+    dev = torch.device("cuda", s.device)
+    tensors = _soa_to_device(gset, dev)
+    n = int(tensors[0].shape[0])
+    rects = torch.zeros((n, 4), dtype=torch.int32, device=dev)
+    depth = torch.zeros((n,), dtype=torch.float64, device=dev)
+    order = torch.zeros((n,), dtype=torch.int32, device=dev)
+    tiles = torch.zeros((n,), dtype=torch.int32, device=dev)
+    nvis = ctypes.c_int64(0)
+    _pre(s)
+    check(s.lib.gsv_project_debug(s.handle, n, int(gset.sh_degree), *(_ptr(t) for t in tensors),
+                                  ctypes.byref(camera_struct(cam)), _ptr(rects), _ptr(depth),
+                                  _ptr(order), _ptr(tiles), ctypes.byref(nvis)))
+    _post(s)
+    return (rects.cpu().numpy(), depth.cpu().numpy(), order.cpu().numpy(), tiles.cpu().numpy(),
+            int(nvis.value))

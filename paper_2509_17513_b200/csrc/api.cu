@@ -1,0 +1,672 @@
+// C ABI entry points (include/gsv_b200.h): sessions, layer-prefix decode of
+// a container into HBM with the reference's validation order, frame
+// materialisation and rendering.
+//
+// read_layers (container.py:260-310) raises the FIRST error met while
+// walking group -> layer -> channel entry -> {read, header, structure,
+// decode+CRC, plane count, valid count}, then the group-level checks of
+// _assemble_frames.  Here the host walks the directory and every payload's
+// structure in that order (stopping at the first structural error, as the
+// reference would), the GPU decodes and CRC-checks every run before that
+// point, and the earliest failure in the reference's order is reported.
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "gsv_internal.h"
+
+using namespace gsv;
+
+struct gsv_session {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    RenderWork work;
+};
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(size_t bytes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = bytes;
+        if (bytes == 0) return GSV_OK;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return fail(GSV_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return GSV_OK;
+    }
+    template <class T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+template <class T>
+int upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
+    int rc = b.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (rc) return rc;
+    if (!v.empty()) GSV_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return GSV_OK;
+}
+
+uint32_t rd32(const uint8_t* p) {
+    uint32_t v;
+    memcpy(&v, p, 4);
+    return v;
+}
+uint16_t rd16(const uint8_t* p) {
+    uint16_t v;
+    memcpy(&v, p, 2);
+    return v;
+}
+
+// An error candidate in the reference's evaluation order.
+struct ErrKey {
+    int64_t order = INT64_MAX;  // entry sequence number (group-level checks after the group's entries)
+    int phase = 0;              // 0 structure, 1 crc, 2 plane count / valid count
+    int kind = GSV_OK;
+    std::string msg;
+    bool set() const { return kind != GSV_OK; }
+    bool before(int64_t o, int ph) const { return !set() || o < order || (o == order && ph < phase); }
+};
+
+// Host-side structural parse of one payload blob (codec.py:80-92, 226-258,
+// 183-223 minus the decoding itself).  Appends the run's PlaneRefs with
+// *offsets* relative to the blob start in `samples`/`coded` (patched to device
+// addresses by the caller).  Returns "" or the CodecError message.
+struct ParsedRun {
+    RunDesc rd{};
+    std::vector<PlaneRef> planes;    // pointers hold blob-relative offsets (+1, 0 = none)
+    std::vector<uint32_t> rc_plane;  // indices (within planes) of range-coded planes
+};
+
+std::string parse_payload(const uint8_t* blob, size_t size, bool check_size, ParsedRun* out) {
+    if (size < 14) return "payload header truncated";
+    const int codec = blob[0], bits = blob[1];
+    const uint32_t w = rd16(blob + 2), h = rd16(blob + 4), count = rd16(blob + 6);
+    const uint32_t length = rd32(blob + 10);
+    const uint64_t end = 14ull + length + 4ull;
+    if (size < end) return "payload body truncated";
+    if (check_size && end != size) return "payload size disagrees with directory";
+    if (bits != 8 && bits != 16 && bits != 32) return "bad bit width " + std::to_string(bits);
+    const uint32_t item = bits / 8;
+    const uint64_t hw = (uint64_t)w * h;
+    const uint64_t plane_bytes = hw * item;
+    const uint64_t expect_raw = (uint64_t)count * plane_bytes;
+    if (plane_bytes > 0xFFFFFFFFull) return "plane too large";
+    RunDesc& r = out->rd;
+    r.checksum = rd32(blob + 14 + length);
+    r.plane_bytes = (uint32_t)plane_bytes;
+    r.w = (uint16_t)w;
+    r.h = (uint16_t)h;
+    r.count = (uint16_t)count;
+    r.bits = (uint8_t)bits;
+    out->planes.clear();
+    out->rc_plane.clear();
+    const uint64_t body = 14;
+    auto raw_run = [&](uint64_t at) {
+        r.kind = 0;
+        for (uint32_t f = 0; f < count; f++) {
+            PlaneRef p{};
+            p.samples = reinterpret_cast<const uint8_t*>(at + f * plane_bytes + 1);
+            p.f = f;
+            p.mode = 1;
+            out->planes.push_back(p);
+        }
+    };
+    if (codec == 0) {
+        if (length != expect_raw) return "raw body length mismatch";
+        raw_run(body);
+        return "";
+    }
+    if (codec == 1) {
+        if (length == 0) return "empty reference-coder body";
+        const int flag = blob[body];
+        const uint64_t coded = body + 1, clen = (uint64_t)length - 1;
+        if (flag == 1) {
+            if (clen != expect_raw) return "raw fallback length mismatch";
+            raw_run(coded);
+            return "";
+        }
+        if (flag != 0) return "unknown body flag " + std::to_string(flag);
+        if (clen < count) return "per-plane mode table truncated";
+        r.kind = 1;
+        uint64_t pos = count;
+        for (uint32_t f = 0; f < count; f++) {
+            const int mode = blob[coded + f];
+            PlaneRef p{};
+            p.f = f;
+            if (mode == 1) {
+                const uint64_t e = pos + plane_bytes;
+                if (e > clen) return "raw plane block truncated";
+                p.samples = reinterpret_cast<const uint8_t*>(coded + pos + 1);
+                p.mode = 1;
+                pos = e;
+            } else if (mode == 0) {
+                if (pos + 4 > clen) return "coded plane length truncated";
+                const uint32_t blen = rd32(blob + coded + pos);
+                pos += 4;
+                const uint64_t e = pos + blen;
+                if (e > clen) return "coded plane block truncated";
+                p.coded = reinterpret_cast<const uint8_t*>(coded + pos + 1);
+                p.coded_len = blen;
+                p.mode = 0;
+                out->rc_plane.push_back(f);
+                pos = e;
+            } else {
+                return "unknown plane mode " + std::to_string(mode);
+            }
+            out->planes.push_back(p);
+        }
+        if (pos != clen) return "trailing bytes after the last plane block";
+        return "";
+    }
+    if (codec == 2) return "external codec payload: no plugin registered";
+    return "unknown codec id " + std::to_string(codec);
+}
+
+// A set of runs resident on the device, decoded and CRC-checked.
+struct RunSet {
+    std::vector<RunDesc> runs;
+    std::vector<PlaneRef> planes;  // device addresses
+    DevBuf d_runs, d_planes, d_planebuf, d_rc, d_chunk, d_crc, d_jobs;
+    std::vector<uint32_t> crc;     // computed CRC per run
+
+    // planes of `pr` (blob-relative) -> device addresses at dev_blob; RC outputs
+    // are assigned later by finalize().
+    void add(ParsedRun& pr, const uint8_t* dev_blob) {
+        RunDesc r = pr.rd;
+        r.plane_base = (uint32_t)planes.size();
+        const uint32_t run_id = (uint32_t)runs.size();
+        for (auto p : pr.planes) {
+            if (p.samples) p.samples = dev_blob + (reinterpret_cast<uintptr_t>(p.samples) - 1);
+            if (p.coded) p.coded = dev_blob + (reinterpret_cast<uintptr_t>(p.coded) - 1);
+            p.run = run_id;
+            planes.push_back(p);
+        }
+        runs.push_back(r);
+    }
+
+    // allocate RC outputs, upload descriptors, decode, CRC, read CRCs back.
+    int decode(cudaStream_t s) {
+        // every plane of a range-coded run gets 16-B aligned storage: RC planes
+        // are decoded there, RAW planes are copied there (aligned predictors)
+        size_t buf = 0;
+        std::vector<size_t> off(planes.size(), 0);
+        for (size_t i = 0; i < planes.size(); i++) {
+            if (runs[planes[i].run].kind == 1) {
+                off[i] = buf;
+                buf += (runs[planes[i].run].plane_bytes + 15) & ~size_t(15);
+            }
+        }
+        int rc = d_planebuf.alloc(buf + 64);
+        if (rc) return rc;
+        std::vector<CopyJob> jobs;
+        for (size_t i = 0; i < planes.size(); i++) {
+            if (runs[planes[i].run].kind != 1) continue;
+            uint8_t* dst = d_planebuf.as<uint8_t>() + off[i];
+            if (planes[i].mode == 1)
+                jobs.push_back(CopyJob{planes[i].samples, dst, runs[planes[i].run].plane_bytes});
+            planes[i].samples = dst;
+        }
+        if ((rc = upload(d_jobs, jobs, s))) return rc;
+        std::vector<uint32_t> rc_runs[3];
+        for (size_t i = 0; i < runs.size(); i++) {
+            if (runs[i].kind != 1) continue;
+            const int nb = runs[i].bits / 8;
+            rc_runs[nb == 1 ? 0 : (nb == 2 ? 1 : 2)].push_back((uint32_t)i);
+        }
+        std::vector<uint32_t> rc_all, rc_start(4, 0);
+        for (int b = 0; b < 3; b++) {
+            rc_start[b] = (uint32_t)rc_all.size();
+            rc_all.insert(rc_all.end(), rc_runs[b].begin(), rc_runs[b].end());
+        }
+        rc_start[3] = (uint32_t)rc_all.size();
+        std::vector<uint32_t> chunk_prefix(planes.size() + 1, 0);
+        for (size_t i = 0; i < planes.size(); i++) {
+            const uint32_t pb = runs[planes[i].run].plane_bytes;
+            chunk_prefix[i + 1] = chunk_prefix[i] + (pb + 1023) / 1024;
+        }
+        if ((rc = upload(d_runs, runs, s))) return rc;
+        if ((rc = upload(d_planes, planes, s))) return rc;
+        if ((rc = upload(d_rc, rc_all, s))) return rc;
+        if ((rc = upload(d_chunk, chunk_prefix, s))) return rc;
+        if ((rc = d_crc.alloc(std::max<size_t>(runs.size(), 1) * 4))) return rc;
+        GSV_CUDA(cudaMemsetAsync(d_crc.p, 0, std::max<size_t>(runs.size(), 1) * 4, s));
+        const int nbytes_of[3] = {1, 2, 4};
+        prof_mark(ST_RCDEC, s);
+        launch_copy_planes(d_jobs.as<CopyJob>(), (int)jobs.size(), s);
+        if (!jobs.empty()) count_launch();
+        for (int b = 0; b < 3; b++) {
+            const int n = (int)(rc_start[b + 1] - rc_start[b]);
+            launch_rc_decode(d_runs.as<RunDesc>(), d_rc.as<uint32_t>() + rc_start[b], n,
+                             d_planes.as<PlaneRef>(), nbytes_of[b], s);
+            if (n > 0) count_launch();
+        }
+        prof_mark(ST_CRC, s);
+        launch_crc(d_runs.as<RunDesc>(), d_planes.as<PlaneRef>(), (int)planes.size(),
+                   d_chunk.as<uint32_t>(), chunk_prefix.back(), d_crc.as<uint32_t>(), s);
+        if (chunk_prefix.back()) count_launch();
+        prof_mark(ST_COUNT, s);
+        crc.assign(runs.size(), 0);
+        if (!runs.empty())
+            GSV_CUDA(cudaMemcpyAsync(crc.data(), d_crc.p, runs.size() * 4, cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        GSV_CUDA(cudaGetLastError());
+        return GSV_OK;
+    }
+};
+
+}  // namespace
+
+struct gsv_video {
+    gsv_session* s = nullptr;
+    Container c;
+    int k = 0;
+    int nslots = 0;
+    DevBuf d_payload;             // staged bytes (empty when resident)
+    RunSet runs;
+    DevBuf d_slots;               // [group][layer][slot]
+    std::vector<size_t> group_slot_base;
+    std::vector<std::vector<uint32_t>> layer_off;  // per group prefix sums
+    int64_t frame_total = 0;
+};
+
+namespace {
+
+int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
+               int up_to_layer, gsv_video** out) {
+    *out = nullptr;
+    gsv_video* v = new gsv_video();
+    v->s = s;
+    auto bail = [&](int rc) {
+        delete v;
+        return rc;
+    };
+    int rc = parse_container(data, len, &v->c);
+    if (rc) return bail(rc);
+    const Container& c = v->c;
+    const int L = c.layer_count;
+    const int k = up_to_layer == -1 ? L : up_to_layer;
+    if (k < 1 || k > L) {
+        return bail(fail(GSV_E_INVALID_INPUT, "layer " + std::to_string(up_to_layer) + " out of range 1.." +
+                                                  std::to_string(L)));
+    }
+    if (k > kMaxLayers) return bail(fail(GSV_E_INVALID_INPUT, "more than 64 layers decoded"));
+    v->k = k;
+    cudaStream_t st = s->stream;
+
+    // ---- stage the layer-prefix bytes of every group -----------------------
+    const int G = (int)c.groups.size();
+    std::vector<uint64_t> lo(G, 0), hi(G, 0), dev_base(G, 0);
+    uint64_t total = 0;
+    for (int g = 0; g < G; g++) {
+        bool any = false;
+        for (int l = 0; l < k; l++)
+            for (const Entry& e : c.groups[g].channels[l]) {
+                if (e.offset >= len) continue;
+                const uint64_t end = std::min<uint64_t>(e.offset + e.size, len);
+                if (!any) {
+                    lo[g] = e.offset;
+                    hi[g] = end;
+                    any = true;
+                } else {
+                    lo[g] = std::min(lo[g], e.offset);
+                    hi[g] = std::max(hi[g], end);
+                }
+            }
+        dev_base[g] = total;
+        total += ((hi[g] - lo[g]) + 15) & ~15ull;
+    }
+    if (!dev_data) {
+        if ((rc = v->d_payload.alloc(total + 64))) return bail(rc);
+        for (int g = 0; g < G; g++)
+            if (hi[g] > lo[g])
+                GSV_CUDA(cudaMemcpyAsync(v->d_payload.as<uint8_t>() + dev_base[g], data + lo[g], hi[g] - lo[g],
+                                         cudaMemcpyHostToDevice, st));
+    }
+    auto dev_addr = [&](int g, uint64_t off) -> const uint8_t* {
+        if (dev_data) return dev_data + off;
+        return v->d_payload.as<uint8_t>() + dev_base[g] + (off - lo[g]);
+    };
+
+    // ---- walk entries in the reference's order ----------------------------
+    const int shdim_ok = c.sh_degree <= 3;
+    const int shdim = shdim_ok ? 3 * (c.sh_degree + 1) * (c.sh_degree + 1) : 0;
+    v->nslots = 11 + shdim;
+    ErrKey stop;     // first structural / group-level error (walk stops there)
+    ErrKey pending;  // first post-CRC error (plane count, valid count)
+    std::vector<int64_t> run_order;            // entry sequence number of each run
+    std::vector<std::string> run_name;         // "group g layer l channel a[c]"
+    struct SlotRef { int run = -1; const Entry* e = nullptr; };
+    std::vector<std::vector<std::vector<SlotRef>>> slots(G);
+    int64_t seq = 0;
+    ParsedRun pr;
+    for (int g = 0; g < G && !stop.set(); g++) {
+        const GroupDir& gd = c.groups[g];
+        slots[g].assign(k, std::vector<SlotRef>(v->nslots));
+        for (int l = 0; l < k && !stop.set(); l++) {
+            const uint32_t n_l = gd.layer_counts[l];
+            for (const Entry& e : gd.channels[l]) {
+                const int64_t o = seq++;
+                char nm[96];
+                snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", g, l + 1, attr_name(e.attr), e.comp);
+                if (e.offset + e.size > len || e.offset > len) {
+                    stop = {o, 0, GSV_E_FORMAT,
+                            "unexpected end of container (wanted " + std::to_string(e.size) + " bytes)"};
+                    break;
+                }
+                std::string m = parse_payload(data + e.offset, e.size, true, &pr);
+                if (!m.empty()) {
+                    stop = {o, 0, GSV_E_CODEC, std::string(nm) + m};
+                    break;
+                }
+                const int run_id = (int)v->runs.runs.size();
+                v->runs.add(pr, dev_addr(g, e.offset));
+                run_order.push_back(o);
+                run_name.push_back(nm);
+                if (pr.rd.count != gd.frame_count) {
+                    if (pending.before(o, 2))
+                        pending = {o, 2, GSV_E_FORMAT,
+                                   std::string(nm) + "expected " + std::to_string(gd.frame_count) +
+                                       " planes, got " + std::to_string(pr.rd.count)};
+                } else if (!(n_l > 0 && (uint64_t)n_l <= (uint64_t)pr.rd.w * pr.rd.h)) {
+                    if (pending.before(o, 2)) pending = {o, 2, GSV_E_INVALID_INPUT, "valid_count out of range"};
+                }
+                const int sl = shdim_ok ? slot_of(e.attr, e.comp, shdim) : -1;
+                if (sl >= 0) slots[g][l][sl] = {run_id, &e};  // later duplicates win (dict semantics)
+            }
+        }
+        if (stop.set()) break;
+        const int64_t o = seq++;  // _assemble_frames of group g
+        if (!shdim_ok) {
+            stop = {o, 0, GSV_E_INVALID_INPUT, "sh_degree must be 0..3, got " + std::to_string(c.sh_degree)};
+            break;
+        }
+        if (gd.frame_count >= 1) {
+            for (int l = 0; l < k && !stop.set(); l++)
+                for (int sl = 0; sl < v->nslots; sl++)
+                    if (slots[g][l][sl].run < 0) {
+                        static const char* an[] = {"position", "rotation", "scales", "opacity", "sh"};
+                        int attr, comp;
+                        if (sl < 3) { attr = 0; comp = sl; }
+                        else if (sl < 7) { attr = 1; comp = sl - 3; }
+                        else if (sl < 10) { attr = 2; comp = sl - 7; }
+                        else if (sl == 10) { attr = 3; comp = 0; }
+                        else { attr = 4; comp = sl - 11; }
+                        stop = {o, 0, GSV_E_FORMAT, std::string("missing channel ") + an[attr] + "[" +
+                                                        std::to_string(comp) + "]"};
+                        break;
+                    }
+        }
+    }
+
+    // ---- decode + CRC on the GPU ------------------------------------------
+    if ((rc = v->runs.decode(st))) return bail(rc);
+    ErrKey best = stop;
+    if (pending.set() && (!best.set() || pending.order < best.order ||
+                          (pending.order == best.order && pending.phase < best.phase)))
+        best = pending;
+    for (size_t r = 0; r < v->runs.runs.size(); r++) {
+        if (v->runs.crc[r] != v->runs.runs[r].checksum) {
+            const int64_t o = run_order[r];
+            if (!best.set() || o < best.order || (o == best.order && 1 < best.phase))
+                best = {o, 1, GSV_E_CODEC, run_name[r] + "checksum mismatch (corrupt or truncated payload)"};
+            break;  // runs are in order: the first mismatch is the earliest
+        }
+    }
+    if (best.set()) return bail(fail(best.kind, best.msg));
+
+    // ---- frame tables ---------------------------------------------------------
+    std::vector<SlotDesc> sd;
+    v->group_slot_base.resize(G);
+    v->layer_off.resize(G);
+    for (int g = 0; g < G; g++) {
+        v->group_slot_base[g] = sd.size();
+        auto& lo2 = v->layer_off[g];
+        lo2.assign(k + 1, 0);
+        for (int l = 0; l < k; l++) {
+            lo2[l + 1] = lo2[l] + c.groups[g].layer_counts[l];
+            for (int sl = 0; sl < v->nslots; sl++) {
+                SlotDesc d{};
+                const SlotRef& ref = slots[g][l][sl];
+                if (ref.run >= 0) {
+                    d.rmin = (double)ref.e->rmin;
+                    d.rmax = (double)ref.e->rmax;
+                    d.plane_base = v->runs.runs[ref.run].plane_base;
+                    d.dir_bits = ref.e->bits;
+                    d.bits = v->runs.runs[ref.run].bits;
+                }
+                sd.push_back(d);
+            }
+        }
+        v->frame_total += c.groups[g].frame_count;
+    }
+    if ((rc = upload(v->d_slots, sd, st))) return bail(rc);
+    GSV_CUDA(cudaStreamSynchronize(st));
+    *out = v;
+    return GSV_OK;
+}
+
+int frame_src(gsv_video* v, int t, FrameSrc* src) {
+    const Container& c = v->c;
+    for (size_t g = 0; g < c.groups.size(); g++) {
+        const GroupDir& gd = c.groups[g];
+        if ((int64_t)gd.start_frame <= t && t < (int64_t)gd.start_frame + gd.frame_count) {
+            memset(src, 0, sizeof *src);
+            src->slots = v->d_slots.as<SlotDesc>() + v->group_slot_base[g];
+            src->planes = v->runs.d_planes.as<PlaneRef>();
+            src->frame = t - (int)gd.start_frame;
+            src->nlayers = v->k;
+            src->nslots = v->nslots;
+            src->sh_degree = c.sh_degree;
+            for (int l = 0; l <= v->k; l++) src->layer_off[l] = v->layer_off[g][l];
+            return GSV_OK;
+        }
+    }
+    return fail(GSV_E_INVALID_INPUT,
+                "frame " + std::to_string(t) + " out of range 0.." + std::to_string(v->frame_total - 1));
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsv_session_create(int device, uintptr_t stream, gsv_session** out) {
+    *out = nullptr;
+    GSV_CUDA(cudaSetDevice(device));
+    gsv_session* s = new gsv_session();
+    s->device = device;
+    if (stream) {
+        s->stream = reinterpret_cast<cudaStream_t>(stream);
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete s;
+            return fail(GSV_E_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+        }
+        s->own_stream = true;
+    }
+    *out = s;
+    return GSV_OK;
+}
+
+void gsv_session_destroy(gsv_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->stream);
+    work_free(&s->work);
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+long long gsv_kernel_launches(void) { return __atomic_load_n(&gsv::g_launches, __ATOMIC_RELAXED); }
+
+int gsv_profile_enable(int enable) {
+    gsv::prof_enable(enable != 0);
+    return GSV_OK;
+}
+
+int gsv_profile_read(double* ms, long long* marks, int max_stages) {
+    return gsv::prof_read(ms, marks, max_stages);
+}
+
+int gsv_session_sync(gsv_session* s) {
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    return GSV_OK;
+}
+
+int gsv_video_open(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer, gsv_video** out) {
+    GSV_CUDA(cudaSetDevice(s->device));
+    return open_video(s, data, len, nullptr, up_to_layer, out);
+}
+
+int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
+                            int up_to_layer, gsv_video** out) {
+    GSV_CUDA(cudaSetDevice(s->device));
+    if (!dev_data) return fail(GSV_E_INVALID_INPUT, "dev_data is NULL");
+    return open_video(s, data, len, dev_data, up_to_layer, out);
+}
+
+void gsv_video_close(gsv_video* v) {
+    if (!v) return;
+    cudaStreamSynchronize(v->s->stream);
+    delete v;
+}
+
+int gsv_video_frame_count(const gsv_video* v) { return (int)v->frame_total; }
+int gsv_video_decoded_layers(const gsv_video* v) { return v->k; }
+
+int gsv_video_group_of(const gsv_video* v, int t) {
+    for (size_t g = 0; g < v->c.groups.size(); g++) {
+        const GroupDir& gd = v->c.groups[g];
+        if ((int64_t)gd.start_frame <= t && t < (int64_t)gd.start_frame + gd.frame_count) return (int)g;
+    }
+    return -1;
+}
+
+int64_t gsv_video_group_splats(const gsv_video* v, int g) {
+    if (g < 0 || g >= (int)v->layer_off.size()) return -1;
+    return v->layer_off[g][v->k];
+}
+
+int gsv_video_frame_values(gsv_video* v, int t, double* pos, double* rot, double* scl, double* opac,
+                           double* sh) {
+    FrameSrc src;
+    int rc = frame_src(v, t, &src);
+    if (rc) return rc;
+    launch_dequant_frame(src, pos, rot, scl, opac, sh, v->s->stream);
+    count_launch();
+    GSV_CUDA(cudaGetLastError());
+    return GSV_OK;
+}
+
+int gsv_video_frame_codes(gsv_video* v, int t, uint32_t* out) {
+    FrameSrc src;
+    int rc = frame_src(v, t, &src);
+    if (rc) return rc;
+    launch_frame_codes(src, out, v->s->stream);
+    count_launch();
+    GSV_CUDA(cudaGetLastError());
+    return GSV_OK;
+}
+
+int gsv_video_render(gsv_video* v, int t, const gsv_camera* cam, float* out_rgb, uint8_t* out_rgb8,
+                     gsv_render_stats* stats) {
+    FrameSrc src;
+    int rc = frame_src(v, t, &src);
+    if (rc) return rc;
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    return render_planes(src, make_cam(*cam), &v->s->work, out_rgb, out_rgb8, stats, v->s->stream);
+}
+
+int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos, const double* rot,
+                   const double* scl, const double* opac, const double* sh, const gsv_camera* cam,
+                   float* out_rgb, uint8_t* out_rgb8, gsv_render_stats* stats) {
+    if (sh_degree < 0 || sh_degree > 3)
+        return fail(GSV_E_INVALID_INPUT, "sh_degree must be 0..3, got " + std::to_string(sh_degree));
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    SoaSrc src{pos, rot, scl, opac, sh, sh_degree, n};
+    return render_soa(src, make_cam(*cam), &s->work, out_rgb, out_rgb8, stats, s->stream);
+}
+
+int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* pos, const double* rot,
+                      const double* scl, const double* opac, const double* sh, const gsv_camera* cam,
+                      int32_t* rects, double* depth, int32_t* order, int32_t* tile_count,
+                      int64_t* n_visible) {
+    if (sh_degree < 0 || sh_degree > 3)
+        return fail(GSV_E_INVALID_INPUT, "sh_degree must be 0..3, got " + std::to_string(sh_degree));
+    SoaSrc src{pos, rot, scl, opac, sh, sh_degree, n};
+    return project_debug(src, make_cam(*cam), &s->work, rects, depth, order, tile_count, n_visible,
+                         s->stream);
+}
+
+int gsv_fold_deltas(gsv_session* s, int64_t n, int shdim, double* pos, double* rot, double* scl,
+                    double* opac, double* sh, int nd, const double* const* d_trans,
+                    const double* const* d_rot, const double* const* d_scl,
+                    const double* const* d_opac, const double* const* d_sh) {
+    if (nd <= 0 || n <= 0) return GSV_OK;
+    int* bad = nullptr;
+    GSV_CUDA(cudaMalloc(&bad, sizeof(int)));
+    cudaMemsetAsync(bad, 0, sizeof(int), s->stream);
+    for (int d = 0; d < nd; d++)
+        launch_fold(n, shdim, pos, rot, scl, opac, sh, d_trans[d], d_rot[d], d_scl[d], d_opac[d], d_sh[d],
+                    bad, s->stream);
+    count_launch(nd);
+    int h = 0;
+    cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
+    cudaError_t e = cudaStreamSynchronize(s->stream);
+    cudaFree(bad);
+    if (e != cudaSuccess) return fail(GSV_E_CUDA, cudaGetErrorString(e));
+    if (h) return fail(GSV_E_INVALID_INPUT, "zero quaternion cannot be normalized");
+    return GSV_OK;
+}
+
+int gsv_decode_payload_host(gsv_session* s, const uint8_t* blob, size_t len, uint32_t* samples,
+                            size_t capacity, int32_t* hdr) {
+    if (len >= 14) {
+        hdr[0] = blob[0];
+        hdr[1] = blob[1];
+        hdr[2] = rd16(blob + 2);
+        hdr[3] = rd16(blob + 4);
+        hdr[4] = rd16(blob + 6);
+    }
+    ParsedRun pr;
+    std::string m = parse_payload(blob, len, false, &pr);
+    if (!m.empty()) return fail(GSV_E_CODEC, m);
+    const size_t nsamp = (size_t)pr.rd.count * pr.rd.w * pr.rd.h;
+    if (nsamp > capacity) return fail(GSV_E_INVALID_INPUT, "output buffer too small");
+    DevBuf d_blob;
+    int rc = d_blob.alloc(len + 64);
+    if (rc) return rc;
+    GSV_CUDA(cudaMemcpyAsync(d_blob.p, blob, len, cudaMemcpyHostToDevice, s->stream));
+    RunSet rs;
+    rs.add(pr, d_blob.as<uint8_t>());
+    if ((rc = rs.decode(s->stream))) return rc;
+    if (rs.crc[0] != rs.runs[0].checksum)
+        return fail(GSV_E_CODEC, "checksum mismatch (corrupt or truncated payload)");
+    // planes -> host u32 samples
+    const uint32_t item = pr.rd.bits / 8, pb = rs.runs[0].plane_bytes;
+    std::vector<uint8_t> tmp((size_t)pb * pr.rd.count + 1);
+    for (uint32_t f = 0; f < pr.rd.count; f++)
+        if (pb) GSV_CUDA(cudaMemcpyAsync(tmp.data() + (size_t)f * pb, rs.planes[f].samples, pb,
+                                         cudaMemcpyDeviceToHost, s->stream));
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    for (size_t i = 0; i < nsamp; i++) {
+        uint32_t x = 0;
+        for (uint32_t b = 0; b < item; b++) x |= (uint32_t)tmp[i * item + b] << (8 * b);
+        samples[i] = x;
+    }
+    return GSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// Internal declarations shared by the libgsv_b200 translation units.
+//
+// Data layout in HBM:
+//   * payload bytes are staged verbatim (one contiguous copy per group
+//     layer-prefix segment, container.py:65-70); codec-0 / raw-fallback /
+//     RAW-mode planes are consumed in place, so decoding them is zero-copy;
+//   * range-coded planes are decoded into `plane_buf` (16-B aligned planes);
+//   * every (run, frame) has a PlaneRef giving the device address of its
+//     little-endian samples, so the projection reads codes straight from the
+//     planes and dequantizes in registers (the fp64 SoA the reference builds,
+//     container.py:229-257, is only materialised on request).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gsv_b200.h"
+
+namespace gsv {
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(int kind, const std::string& msg);
+int fail(int kind, const std::string& msg);
+#define GSV_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess)                                                      \
+            return ::gsv::fail(GSV_E_CUDA, std::string(#call) + ": " +              \
+                                               cudaGetErrorString(e_));             \
+    } while (0)
+
+// ---- container directory (container.py:35-41, 151-191) ----------------------
+struct Entry {
+    uint8_t attr;      // 0 position, 1 rotation, 2 scales, 3 opacity, 4 sh
+    uint16_t comp;
+    uint8_t bits;      // directory bit width (used for dequantization)
+    uint64_t offset;
+    uint64_t size;
+    float rmin, rmax;
+};
+
+struct GroupDir {
+    uint32_t start_frame;
+    uint16_t frame_count;
+    uint8_t position_bits;
+    std::vector<uint32_t> layer_counts;
+    std::vector<std::vector<Entry>> channels;  // [layer][entry]
+};
+
+struct Container {
+    uint16_t version = 0;
+    uint8_t layer_count = 0;
+    uint8_t sh_degree = 0;
+    uint16_t fps_num = 0, fps_den = 0;
+    float bounds[6] = {0};
+    uint32_t flags = 0;
+    std::vector<GroupDir> groups;
+    uint64_t header_bytes = 0;  // header + directory
+};
+
+int parse_container(const uint8_t* data, size_t len, Container* out);
+const char* attr_name(int attr);
+
+// slot of (attr, comp) in the per-splat attribute vector:
+// position 0-2, rotation 3-6, scales 7-9, opacity 10, sh 11.. ; -1 if unused
+int slot_of(int attr, int comp, int shdim);
+inline int slot_count(int sh_degree) { return 11 + 3 * (sh_degree + 1) * (sh_degree + 1); }
+constexpr int kMaxSlots = 11 + 48;
+constexpr int kMaxLayers = 64;
+
+// ---- device descriptors ------------------------------------------------------
+// One decodable (group, layer, entry) payload.
+struct RunDesc {
+    uint32_t checksum;
+    uint32_t plane_bytes;  // h*w*item
+    uint32_t plane_base;   // first PlaneRef of this run
+    uint16_t w, h, count;
+    uint8_t bits;          // payload bit width
+    uint8_t kind;          // 0: raw samples in place, 1: per-plane (codec 1, flag 0)
+};
+
+// One plane of one run.
+struct PlaneRef {
+    const uint8_t* samples;  // little-endian samples (device; may be unaligned)
+    const uint8_t* coded;    // range-coded block (mode 0) or nullptr
+    uint32_t coded_len;
+    uint32_t run;
+    uint32_t f;              // index inside the run
+    uint32_t mode;           // 0: range coded, 1: raw
+};
+
+// Per (group, layer, slot) dequantization parameters + the run providing it.
+struct SlotDesc {
+    double rmin, rmax;      // directory range (f32 values promoted)
+    uint32_t plane_base;    // PlaneRef index of frame 0 of the run
+    uint8_t dir_bits;       // directory bit width -> top = 2^bits - 1
+    uint8_t bits;           // payload sample width
+    uint16_t pad;
+};
+
+// A frame's source: `nlayers` layers of its group.
+struct FrameSrc {
+    const SlotDesc* slots;       // [nlayers][nslots] for the frame's group
+    const PlaneRef* planes;      // all PlaneRefs
+    int32_t frame;               // frame index inside its group
+    int32_t nlayers;
+    int32_t nslots;
+    int32_t sh_degree;
+    uint32_t layer_off[kMaxLayers + 1];  // prefix sums of layer counts
+};
+
+// fp64 SoA source (render_set / render_progressive inputs)
+struct SoaSrc {
+    const double* pos;   // (n,3)
+    const double* rot;   // (n,4)
+    const double* scl;   // (n,3)
+    const double* opac;  // (n)
+    const double* sh;    // (n,shdim)
+    int32_t sh_degree;
+    int64_t n;
+};
+
+// Camera as the kernels see it (render.py:43-120)
+struct CamDev {
+    double R[9];
+    double t[3];
+    double center[3];
+    double fx, fy, cx, cy, near_;
+    float bg[3];
+    int32_t width, height;
+};
+
+// 48-byte splat record consumed by the compositor (all fp32):
+//   ox, oy : mean - rect origin (px)       ca, cb, cc : conic inverse (render.py:346-349)
+//   r, g, b: SH colour in [0,1]             op : opacity
+//   rx, ry : x0 | x1 << 16, y0 | y1 << 16   (u16 each)
+struct __align__(16) SplatRec {
+    float ox, oy, ca, cb;
+    float cc, r, g, b;
+    float op;
+    uint32_t rx, ry;
+    uint32_t pad;
+};
+
+// ---- workspace for one in-flight render ----------------------------------
+struct RenderWork {
+    int64_t cap_n = 0;    // splat capacity
+    int64_t cap_k = 0;    // key capacity
+    int cap_tiles = 0;
+    // per splat
+    uint64_t* dkey[2] = {nullptr, nullptr};  // depth sort keys (ping-pong)
+    uint32_t* didx[2] = {nullptr, nullptr};  // splat indices (ping-pong)
+    SplatRec* rec = nullptr;                 // by splat index
+    SplatRec* rec_sorted = nullptr;          // by depth rank
+    uint32_t* cnt = nullptr;                 // tile count by rank -> exclusive offsets
+    // per key
+    uint32_t* tkey[2] = {nullptr, nullptr};
+    uint32_t* tval[2] = {nullptr, nullptr};
+    // per tile
+    uint32_t* range = nullptr;               // [tiles][2]
+    // radix / scan scratch
+    uint32_t* hist = nullptr;
+    int64_t hist_cap = 0;
+    // device counters: [0] n_visible, [1] n_keys, [2..3] depth min (u64), [4..5] depth max,
+    // [6] key overflow flag, [8..] radix pass state
+    unsigned long long* ctr = nullptr;
+    unsigned long long* h_ctr = nullptr;     // pinned mirror
+};
+
+int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles);
+void work_free(RenderWork* w);
+
+// byte copy job (RAW planes of range-coded runs -> aligned storage)
+struct CopyJob {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+};
+
+// ---- kernels (host launchers) -------------------------------------------------
+// rc_decode.cu
+void launch_copy_planes(const CopyJob* jobs, int njobs, cudaStream_t s);
+// decode.cu
+void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, int n_rc_runs,
+                      const PlaneRef* planes, int nbytes, cudaStream_t s);
+void launch_crc(const RunDesc* runs, const PlaneRef* planes, int nplanes,
+                const uint32_t* plane_chunk_prefix, uint32_t nchunks, uint32_t* run_crc,
+                cudaStream_t s);
+void launch_dequant_frame(const FrameSrc& src, double* pos, double* rot, double* scl,
+                          double* opac, double* sh, cudaStream_t s);
+void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
+
+// render.cu: full per-frame pipeline
+int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+                  uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
+int render_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+               uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
+int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
+                  double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
+                  cudaStream_t s);
+void launch_fold(int64_t n, int shdim, double* pos, double* rot, double* scl, double* opac,
+                 double* sh, const double* dt, const double* dq, const double* ds,
+                 const double* dop, const double* dsh, int* bad, cudaStream_t s);
+
+CamDev make_cam(const gsv_camera& c);
+constexpr int kTile = 16;
+
+// ---- launch accounting and stage profiling (bench instrumentation) ---------
+extern long long g_launches;  // kernels launched by this library (all threads)
+inline void count_launch(int n = 1) { __atomic_fetch_add(&g_launches, (long long)n, __ATOMIC_RELAXED); }
+
+enum Stage { ST_PROJECT = 0, ST_DSORT, ST_EMIT, ST_TSORT, ST_RANGES, ST_COMPOSITE, ST_RCDEC, ST_CRC,
+             ST_COUNT };
+// When enabled, mark(stage) records an event on the stream; the interval up to
+// the next mark is charged to `stage` (ST_COUNT = idle / end).
+void prof_mark(int stage, cudaStream_t s);
+void prof_enable(bool on);
+int prof_read(double* ms, long long* marks, int max_stages);
+
+}  // namespace gsv

@@ -1,0 +1,340 @@
+// Per-frame render pipeline: project -> depth rank sort -> tile key emission
+// -> tile sort -> tile ranges -> composite.  Everything is enqueued on one
+// stream with counts kept on the device, so a frame needs no host round trip
+// (the host only reads the counters back when asked for statistics or to
+// detect a key-buffer overflow).
+//
+// Ordering contract (render.py:342-356): splats are composited in the order
+// of np.argsort(depth, kind="stable") over project_set's survivors.  The
+// depth sort below is a stable LSD radix sort of the fp64 depth bit patterns
+// (depth > near > 0, so unsigned order == numeric order) with the splat index
+// as payload over *all* splats in index order, culled splats keyed past the
+// largest survivor: its first n_visible entries are exactly that order.  Tile
+// keys are then emitted in rank order and stably sorted by tile, so every
+// tile sees its splats in global depth-rank order.
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "gsv_internal.h"
+#include "sort.cuh"
+
+namespace gsv {
+
+void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
+void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* dbg_rect,
+                        double* dbg_depth, cudaStream_t s);
+void launch_composite(const uint32_t* ranks, const uint32_t* range, const SplatRec* recs,
+                      const CamDev& cam, float* out_rgb, uint8_t* out_rgb8, cudaStream_t s);
+
+enum { C_NVIS = 0, C_NKEYS = 1, C_DMIN = 2, C_DMAX = 3, C_OVF = 4, C_N = 5, C_KCLAMP = 6,
+       C_NPASS = 8 /* int */ };
+
+CamDev make_cam(const gsv_camera& c) {
+    CamDev d;
+    memcpy(d.R, c.rotation, sizeof d.R);
+    memcpy(d.t, c.translation, sizeof d.t);
+    // center = -R^T @ t (render.py:74-77), evaluated like BLAS gemv
+    for (int i = 0; i < 3; i++) {
+        const double m0 = -c.rotation[0 * 3 + i], m1 = -c.rotation[1 * 3 + i], m2 = -c.rotation[2 * 3 + i];
+        d.center[i] = fma(m2, c.translation[2], fma(m1, c.translation[1], m0 * c.translation[0]));
+    }
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    d.near_ = c.near_plane;
+    for (int k = 0; k < 3; k++) d.bg[k] = (float)c.background[k];
+    d.width = c.width;
+    d.height = c.height;
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void reset_ctr_kernel(unsigned long long* ctr, long long n) {
+    ctr[C_NVIS] = 0;
+    ctr[C_NKEYS] = 0;
+    ctr[C_DMIN] = ~0ull;
+    ctr[C_DMAX] = 0;
+    ctr[C_OVF] = 0;
+    ctr[C_N] = (unsigned long long)n;
+    ctr[C_KCLAMP] = 0;
+    ctr[7] = 0;
+    reinterpret_cast<int*>(ctr + C_NPASS)[0] = 0;
+}
+
+// Rebase survivor depth bits to [0, range]; culled splats get range + 1.
+// Passes needed = bytes spanned by range + 1.
+__global__ void depth_key_prep(uint64_t* __restrict__ key, unsigned long long* __restrict__ ctr) {
+    const uint64_t n = ctr[C_N];
+    const uint64_t nvis = ctr[C_NVIS];
+    const uint64_t lo = ctr[C_DMIN], hi = ctr[C_DMAX];
+    const uint64_t dead = nvis ? (hi - lo) + 1 : 0;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        int bits = dead ? 64 - __clzll((long long)dead) : 0;
+        reinterpret_cast<int*>(ctr + C_NPASS)[0] = (nvis == 0 || nvis == n && hi == lo) ? 0 : (bits + 7) / 8;
+    }
+    if (i < n) {
+        const uint64_t k = key[i];
+        key[i] = (k == ~0ull) ? dead : k - lo;
+    }
+}
+
+__device__ __forceinline__ uint32_t rec_tile_count(const SplatRec& r) {
+    const uint32_t x0 = r.rx & 0xFFFFu, x1 = r.rx >> 16, y0 = r.ry & 0xFFFFu, y1 = r.ry >> 16;
+    return ((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1);
+}
+
+// rank r -> record in rank order + its tile count
+__global__ void emit_prep(const SplatRec* __restrict__ rec,
+                          SplatRec* __restrict__ rec_sorted, uint32_t* __restrict__ cnt,
+                          const unsigned long long* __restrict__ ctr, uint32_t* didx0,
+                          uint32_t* didx1) {
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
+    const uint32_t* idx = (np & 1) ? didx1 : didx0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nvis; r += gridDim.x * blockDim.x) {
+        const SplatRec s = rec[idx[r]];
+        rec_sorted[r] = s;
+        cnt[r] = rec_tile_count(s);
+    }
+}
+
+// scatter (tile, rank) keys in rank order
+__global__ void emit_keys(const SplatRec* __restrict__ rec_sorted, const uint32_t* __restrict__ off,
+                          unsigned long long* __restrict__ ctr, uint32_t* __restrict__ tkey,
+                          uint32_t* __restrict__ tval, uint64_t cap, int ntx) {
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const uint64_t K = ctr[C_NKEYS];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr[C_KCLAMP] = K < cap ? K : cap;
+        if (K > cap) ctr[C_OVF] = K;
+    }
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nvis; r += gridDim.x * blockDim.x) {
+        const SplatRec s = rec_sorted[r];
+        const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
+        const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
+        uint64_t o = off[r];
+        for (uint32_t ty = y0; ty <= y1; ty++)
+            for (uint32_t tx = x0; tx <= x1; tx++, o++) {
+                if (o < cap) {
+                    tkey[o] = ty * (uint32_t)ntx + tx;
+                    tval[o] = r;
+                }
+            }
+    }
+}
+
+__global__ void tile_ranges(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ ctr,
+                            uint32_t* __restrict__ range) {
+    const uint32_t K = (uint32_t)ctr[C_KCLAMP];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+        const uint32_t t = key[i];
+        if (i == 0 || key[i - 1] != t) range[2 * t] = i;
+        if (i == K - 1 || key[i + 1] != t) range[2 * t + 1] = i + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+static void free_ptr(void* p) {
+    if (p) cudaFree(p);
+}
+
+void work_free(RenderWork* w) {
+    for (int b = 0; b < 2; b++) {
+        free_ptr(w->dkey[b]);
+        free_ptr(w->didx[b]);
+        free_ptr(w->tkey[b]);
+        free_ptr(w->tval[b]);
+    }
+    free_ptr(w->rec);
+    free_ptr(w->rec_sorted);
+    free_ptr(w->cnt);
+    free_ptr(w->range);
+    free_ptr(w->hist);
+    free_ptr(w->ctr);
+    if (w->h_ctr) cudaFreeHost(w->h_ctr);
+    *w = RenderWork();
+}
+
+int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles) {
+    if (!w->ctr) {
+        GSV_CUDA(cudaMalloc(&w->ctr, 16 * sizeof(unsigned long long)));
+        GSV_CUDA(cudaMallocHost(&w->h_ctr, 16 * sizeof(unsigned long long)));
+    }
+    n = std::max<int64_t>(n, 1);
+    if (n > w->cap_n) {
+        const int64_t c = std::max<int64_t>(n, w->cap_n * 5 / 4);
+        for (int b = 0; b < 2; b++) {
+            free_ptr(w->dkey[b]);
+            free_ptr(w->didx[b]);
+            GSV_CUDA(cudaMalloc(&w->dkey[b], c * sizeof(uint64_t)));
+            GSV_CUDA(cudaMalloc(&w->didx[b], c * sizeof(uint32_t)));
+        }
+        free_ptr(w->rec);
+        free_ptr(w->rec_sorted);
+        free_ptr(w->cnt);
+        GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
+        GSV_CUDA(cudaMalloc(&w->rec_sorted, c * sizeof(SplatRec)));
+        GSV_CUDA(cudaMalloc(&w->cnt, (c + 1) * sizeof(uint32_t)));
+        w->cap_n = c;
+    }
+    k = std::max<int64_t>(k, 1 << 16);
+    if (k > w->cap_k) {
+        const int64_t c = std::max<int64_t>(k, w->cap_k * 5 / 4);
+        for (int b = 0; b < 2; b++) {
+            free_ptr(w->tkey[b]);
+            free_ptr(w->tval[b]);
+            GSV_CUDA(cudaMalloc(&w->tkey[b], c * sizeof(uint32_t)));
+            GSV_CUDA(cudaMalloc(&w->tval[b], c * sizeof(uint32_t)));
+        }
+        w->cap_k = c;
+    }
+    if (tiles > w->cap_tiles) {
+        free_ptr(w->range);
+        GSV_CUDA(cudaMalloc(&w->range, (size_t)tiles * 2 * sizeof(uint32_t)));
+        w->cap_tiles = tiles;
+    }
+    const int64_t hw = std::max(radix_hist_words(std::max(w->cap_n, w->cap_k)),
+                                scan_bsum_words(w->cap_n)) + 512;
+    if (hw > w->hist_cap) {
+        free_ptr(w->hist);
+        GSV_CUDA(cudaMalloc(&w->hist, hw * sizeof(uint32_t)));
+        w->hist_cap = hw;
+    }
+    return GSV_OK;
+}
+
+static int tile_passes(int ntiles) {
+    int bits = 0;
+    while ((1 << bits) < ntiles) bits++;
+    return std::max(1, (bits + 7) / 8);
+}
+
+// Enqueue one frame.  `project` enqueues the projection kernel into w.
+template <class Proj>
+static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj project,
+                          float* out_rgb, uint8_t* out_rgb8, cudaStream_t s) {
+    const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
+    const int ntiles = ntx * nty;
+    if (cam.width > 65535 || cam.height > 65535) return fail(GSV_E_INVALID_INPUT, "image too large");
+    int rc = work_reserve(w, n, std::max<int64_t>(w->cap_k, 16 * n), ntiles);
+    if (rc) return rc;
+    unsigned long long* ctr = w->ctr;
+    int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
+    uint32_t* digit_total = w->hist + (w->hist_cap - 512);
+    prof_mark(ST_PROJECT, s);
+    reset_ctr_kernel<<<1, 1, 0, s>>>(ctr, (long long)n);
+    project();
+    count_launch(2);
+    prof_mark(ST_DSORT, s);
+    if (n > 0) {
+        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], ctr);
+        radix_sort<uint64_t>(w->dkey, w->didx, ctr + C_N, w->cap_n, 8, npass, w->hist, digit_total, s);
+        count_launch(1 + 3 * 8);
+    }
+    prof_mark(ST_EMIT, s);
+    const unsigned g = 148 * 8;
+    emit_prep<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, w->cnt, ctr, w->didx[0], w->didx[1]);
+    exclusive_scan(w->cnt, ctr + C_NVIS, w->cap_n, w->hist, ctr + C_NKEYS, s);
+    emit_keys<<<g, 256, 0, s>>>(w->rec_sorted, w->cnt, ctr, w->tkey[0], w->tval[0],
+                                (uint64_t)w->cap_k, ntx);
+    count_launch(5);
+    prof_mark(ST_TSORT, s);
+    const int tp = tile_passes(ntiles);
+    radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, w->hist, digit_total, s);
+    count_launch(3 * tp);
+    prof_mark(ST_RANGES, s);
+    cudaMemsetAsync(w->range, 0, (size_t)ntiles * 2 * sizeof(uint32_t), s);
+    tile_ranges<<<g, 256, 0, s>>>(w->tkey[tp & 1], ctr, w->range);
+    count_launch(1);
+    prof_mark(ST_COMPOSITE, s);
+    launch_composite(w->tval[tp & 1], w->range, w->rec_sorted, cam, out_rgb, out_rgb8, s);
+    count_launch(1);
+    prof_mark(ST_COUNT, s);
+    cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    GSV_CUDA(cudaGetLastError());
+    return GSV_OK;
+}
+
+// Enqueue, then check the key capacity; on overflow grow and re-render.
+template <class Proj>
+static int render_checked(int64_t n, const CamDev& cam, RenderWork* w, Proj project, float* out_rgb,
+                          uint8_t* out_rgb8, gsv_render_stats* st, cudaStream_t s) {
+    for (int attempt = 0; attempt < 4; attempt++) {
+        int rc = render_enqueue(n, cam, w, project, out_rgb, out_rgb8, s);
+        if (rc) return rc;
+        GSV_CUDA(cudaStreamSynchronize(s));
+        const unsigned long long K = w->h_ctr[C_NKEYS];
+        if (w->h_ctr[C_OVF] == 0) {
+            if (st) {
+                st->n_splats = n;
+                st->n_visible = (int64_t)w->h_ctr[C_NVIS];
+                st->n_keys = (int64_t)K;
+                st->tiles_x = (cam.width + kTile - 1) / kTile;
+                st->tiles_y = (cam.height + kTile - 1) / kTile;
+            }
+            return GSV_OK;
+        }
+        rc = work_reserve(w, n, (int64_t)(K + K / 4 + 1024), 0);
+        if (rc) return rc;
+    }
+    return fail(GSV_E_NOMEM, "tile key buffer could not be sized");
+}
+
+int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+                  uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s) {
+    const int64_t n = src.layer_off[src.nlayers];
+    auto proj = [&]() { launch_project_planes(src, cam, w, s); };
+    if (stats == reinterpret_cast<gsv_render_stats*>(1)) {  // enqueue only (throughput mode)
+        return render_enqueue(n, cam, w, proj, out_rgb, out_rgb8, s);
+    }
+    return render_checked(n, cam, w, proj, out_rgb, out_rgb8, stats, s);
+}
+
+int render_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+               uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s) {
+    auto proj = [&]() { launch_project_soa(src, cam, w, nullptr, nullptr, s); };
+    return render_checked(src.n, cam, w, proj, out_rgb, out_rgb8, stats, s);
+}
+
+__global__ void copy_order(const uint32_t* __restrict__ idx0, const uint32_t* __restrict__ idx1,
+                           const unsigned long long* __restrict__ ctr, int32_t* __restrict__ order,
+                           const SplatRec* __restrict__ rec, int32_t* __restrict__ tile_count) {
+    const uint64_t n = ctr[C_N];
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
+    const uint32_t* idx = (np & 1) ? idx1 : idx0;
+    for (uint64_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t i = idx[r];
+        order[r] = (int32_t)i;
+        if (tile_count) tile_count[i] = r < nvis ? (int32_t)rec_tile_count(rec[i]) : 0;
+    }
+}
+
+int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
+                  double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
+                  cudaStream_t s) {
+    const int64_t n = src.n;
+    int rc = work_reserve(w, n, w->cap_k, 1);
+    if (rc) return rc;
+    unsigned long long* ctr = w->ctr;
+    int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
+    uint32_t* digit_total = w->hist + (w->hist_cap - 512);
+    reset_ctr_kernel<<<1, 1, 0, s>>>(ctr, (long long)n);
+    launch_project_soa(src, cam, w, rects, depth, s);
+    if (n > 0) {
+        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], ctr);
+        radix_sort<uint64_t>(w->dkey, w->didx, ctr + C_N, w->cap_n, 8, npass, w->hist, digit_total, s);
+        copy_order<<<148 * 4, 256, 0, s>>>(w->didx[0], w->didx[1], ctr, order, w->rec, tile_count);
+    }
+    cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    GSV_CUDA(cudaStreamSynchronize(s));
+    GSV_CUDA(cudaGetLastError());
+    if (n_visible) *n_visible = (int64_t)w->h_ctr[C_NVIS];
+    return GSV_OK;
+}
+
+}  // namespace gsv

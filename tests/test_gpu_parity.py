@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): bit-exact for dequantized integer symbols /
+fp64 values, group assignment, rects, tile counts and depth order; images
+within max-abs 2e-3 per channel and |dPSNR| <= 0.01 dB.
+"""
+
+import base64
+import json
+
+import numpy as np
+import pytest
+
+from golden_util import (GOLDEN, Cam, camera, container, doc, progressive_inputs, renders,
+                         scene_names, set_sha)
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-3
+MAX_DPSNR = 0.01
+
+
+@pytest.fixture(scope="module")
+def gsvb():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2509_17513_b200 as m
+    return m
+
+
+def test_native_library_is_loaded(gsvb):
+    from paper_2509_17513_b200 import _lib
+    L = _lib.load()
+    maps = open("/proc/self/maps").read()
+    assert str(_lib.LIB_PATH) in maps
+
+
+@pytest.mark.parametrize("path", sorted((GOLDEN / "conformance").glob("*.json")),
+                         ids=lambda p: p.stem)
+def test_conformance_payloads_gpu(gsvb, path):
+    d = json.loads(path.read_text())
+    blob = base64.b64decode(d["payload_b64"])
+    payload, end = gsvb.CodedPayload.from_bytes(blob)
+    assert end == len(blob)
+    planes = gsvb.decode_planes(payload)
+    assert len(planes) == d["count"]
+    for plane, exp in zip(planes, d["expected_samples"]):
+        assert plane.samples.ravel().tolist() == exp
+
+
+def test_decode_planes_corruption_gpu(gsvb):
+    d = json.loads((GOLDEN / "conformance" / "rc_u8_random.json").read_text())
+    blob = bytearray(base64.b64decode(d["payload_b64"]))
+    blob[20] ^= 0x04
+    payload, _ = gsvb.CodedPayload.from_bytes(bytes(blob))
+    with pytest.raises(gsvb.CodecError):
+        gsvb.decode_planes(payload)
+
+
+@pytest.mark.parametrize("name", scene_names())
+def test_decode_bit_exact_and_group_assignment(gsvb, name):
+    sc = doc()["scenes"][name]
+    data = container(name)
+    for k in range(1, sc["layer_count"] + 1):
+        with gsvb.DeviceVideo(data, k) as v:
+            assert v.frame_count == sum(g["frames"] for g in sc["groups"])
+            info = O.read_structure(data)
+            for t in range(v.frame_count):
+                assert v.group_of(t) == O.group_of(info, t)
+                assert set_sha(v.frame(t)) == sc["decode"][str(k)][t], (name, k, t)
+            # integer symbols against the oracle's decode
+            _, _ = O.read_layers(data, k)
+            gi = v.group_of(0)
+            vals = O.decode_group_codes(data, info, gi, k)
+            codes = v.frame_codes(0).cpu().numpy().astype(np.uint32)
+            deg = info.sh_degree
+            order = [("position", c) for c in range(3)] + [("rotation", c) for c in range(4)] + \
+                [("scales", c) for c in range(3)] + [("opacity", 0)] + \
+                [("sh", c) for c in range(3 * (deg + 1) ** 2)]
+            exp = np.concatenate([np.stack([vals[l][key][0][0] for key in order], axis=1)
+                                  for l in range(k)])
+            assert np.array_equal(codes, exp)
+
+
+@pytest.mark.parametrize("name", scene_names())
+def test_render_matches_reference_images(gsvb, name):
+    sc = doc()["scenes"][name]
+    data = container(name)
+    arr = renders(name)
+    for key, r in sc["renders"].items():
+        cam = camera(name, r["cam"])
+        with gsvb.DeviceVideo(data, r["k"]) as v:
+            img, st = v.render(r["t"], cam, stats=True)
+            got = img.cpu().numpy().astype(np.float64)
+            g = v.frame(r["t"])
+        ref = arr[f"{key}_img"]
+        err = float(np.max(np.abs(got - ref)))
+        assert err <= MAX_ABS, (key, err)
+        # counts are bit-exact: survivors and tile keys from the reference rects
+        rects = arr[f"{key}_rects"]
+        assert st["n_visible"] == rects.shape[0]
+        assert st["n_keys"] == int(O.tile_counts(rects).sum())
+        # projection: rects, depth, order, tile counts exact
+        prect, pdepth, porder, ptiles, nvis = gsvb.project_debug(g, cam)
+        idx = arr[f"{key}_idx"]
+        assert nvis == idx.size
+        assert np.array_equal(prect[idx].astype(np.int64), rects)
+        assert np.array_equal(pdepth[idx], arr[f"{key}_depth"])
+        assert np.array_equal(porder[:nvis], idx[arr[f"{key}_order"]])
+        assert np.array_equal(ptiles[idx], O.tile_counts(rects))
+
+
+def test_error_paths_match_reference(gsvb):
+    errs = doc()["errors"]
+    blob = container(errs["container"])
+    classes = {"CodecError": gsvb.CodecError, "FormatError": gsvb.FormatError,
+               "InvalidInputError": gsvb.InvalidInputError}
+    for case in errs["cases"]:
+        data = bytearray(blob)
+        if case["kind"] == "flip":
+            data[case["offset"]] ^= 1 << case["bit"]
+        elif case["kind"] == "truncate":
+            data = data[:case["length"]]
+        if case["error"] is None:
+            gsvb.DeviceVideo(bytes(data), case["k"]).close()
+            continue
+        with pytest.raises(classes[case["error"]]) as ei:
+            gsvb.DeviceVideo(bytes(data), case["k"])
+        assert str(ei.value) == case["message"], case
+
+
+def test_progressive_matches_reference(gsvb):
+    layers, deltas, cam, d, a = progressive_inputs()
+    frame = gsvb.LayeredFrame(layers=tuple(layers), layer_fractions=(0.3, 0.3, 0.4),
+                              volume_weight=1e5)
+    for key, c in d["cases"].items():
+        g = gsvb.reconstruct_frame(frame, deltas, c["t"], c["k"])
+        for nm in ("positions", "rotations", "scales", "opacities", "sh"):
+            assert np.array_equal(getattr(g, nm), a[f"recon_{key}_{nm}"]), (key, nm)
+        img = gsvb.render_progressive(frame, c["k"], deltas, c["t"], cam)
+        assert np.max(np.abs(img.pixels - a[f"img_{key}"])) <= MAX_ABS, key
+    with pytest.raises(gsvb.InvalidInputError, match="layer 4 out of range 1..3"):
+        gsvb.render_progressive(frame, 4, deltas, 0, cam)
+
+
+def test_acceptance_scenes(gsvb):
+    from paper_2509_17513_b200.synth import SceneSpec, iter_frames
+    ka = doc()["known_answer"]
+    arr = renders("known_answer")
+    for i, sc in enumerate(ka["accept"]):
+        g = next(iter_frames(SceneSpec(count=300, frames=1, sh_degree=1,
+                                       scale_range=(0.02, 0.08)), sc["seed"]))
+        cam = Cam.from_json(sc["camera"])
+        img = gsvb.render_set(g, cam)
+        assert np.max(np.abs(img.pixels - arr[f"accept{i}_img"])) <= MAX_ABS
+
+
+def _bench_scene(count, frames, group_len, layers, codec, seed):
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    spec = benchmark_spec(count, frames, group_len)
+    cfg = EncodeConfig(layer_count=layers, prune_fraction=0.0, codec=codec)
+    return encode_stream(lambda: iter_frames(spec, seed), cfg, codecs=(0, 1)), spec
+
+
+def _psnr(a, b):
+    return O.psnr(a, b)
+
+
+def test_config1_full_parity(gsvb):
+    """BASELINE config 1: 50k Gaussians, 2 layers, 4 frames (2 groups), 512^2,
+    both codecs, every frame and prefix, axis + oblique cameras."""
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    blobs, spec = _bench_scene(50_000, 4, 2, 2, 1, 1001)
+    assert blobs[0] != blobs[1]
+    frames_src = list(iter_frames(spec, 1001))
+    for cname, cam in (("axis", Cam.from_json(_cam_json(512, 512, (0, 0, -2.5)))),
+                       ("oblique", Cam.from_json(_cam_json(512, 512, (1.3, 0.9, -1.9))))):
+        for codec in (0, 1):
+            data = blobs[codec]
+            for k in (1, 2):
+                _, groups = O.read_layers(data, k)
+                with gsvb.DeviceVideo(data, k) as v:
+                    for t in range(4):
+                        g = O.frame_of(groups, t)
+                        img = v.render(t, cam).cpu().numpy().astype(np.float64)
+                        ref = O.render_set(g, cam)
+                        assert np.max(np.abs(img - ref)) <= MAX_ABS, (codec, k, t, cname)
+                        if codec == 1 and k == 2:
+                            gt = O.render_set(frames_src[t], cam)
+                            assert abs(_psnr(gt, img) - _psnr(gt, ref)) <= MAX_DPSNR
+
+
+def _cam_json(w, h, eye):
+    from paper_2509_17513_b200.types import Camera
+    return Camera.looking_at(eye=eye, target=(0, 0, 0), fov_deg=60.0, width=w, height=h,
+                             near=0.01).to_json_dict()
+
+
+def test_config2_frame_parity(gsvb):
+    """BASELINE config 2 geometry: 300k Gaussians, 6 layers, 1080p; two frames
+    (one group) checked against the oracle at k = 1 and 6."""
+    blobs, spec = _bench_scene(300_000, 2, 30, 6, 1, 1002)
+    cam = Cam.from_json(_cam_json(1920, 1080, (0, 0, -2.5)))
+    data = blobs[1]
+    for k in (1, 6):
+        _, groups = O.read_layers(data, k)
+        with gsvb.DeviceVideo(data, k) as v:
+            for t in (0, 1):
+                g = O.frame_of(groups, t)
+                img, st = v.render(t, cam, stats=True)
+                img = img.cpu().numpy().astype(np.float64)
+                means, covs, depth, colors, opac, rects, idx = O.project_set(g, cam)
+                ref = O.composite(means, covs, depth, colors, opac, rects, cam)
+                assert st["n_visible"] == idx.size
+                assert st["n_keys"] == int(O.tile_counts(rects).sum())
+                assert np.max(np.abs(img - ref)) <= MAX_ABS, (k, t)
