@@ -84,8 +84,9 @@ typedef struct gsv_entry_info { /* container.py:44-51 */
 typedef struct gsv_render_stats {
     int64_t n_splats;   /* splats projected (layer prefix size) */
     int64_t n_visible;  /* survivors of project_set's culls */
-    int64_t n_keys;     /* (tile, rank) keys emitted */
+    int64_t n_keys;     /* (tile, splat) overlaps of the visible splats */
     int32_t tiles_x, tiles_y;
+    int64_t n_keys_emitted; /* keys actually emitted (saturated tiles get none in later rounds) */
 } gsv_render_stats;
 
 const char* gsv_last_error(void);
@@ -140,6 +141,18 @@ int gsv_video_frame_codes(gsv_video* v, int t, uint32_t* out);
  * rounded like write_ppm (render.py:165-169).  Either output may be NULL. */
 int gsv_video_render(gsv_video* v, int t, const gsv_camera* cam, float* out_rgb,
                      uint8_t* out_rgb8, gsv_render_stats* stats);
+/* Render `count` frames of v (frames[j]) frame-parallel on `nstreams`
+ * auxiliary streams (joined back into the session stream).  Per frame j:
+ * out_rgb[j] (device fp32), out_rgb8[j] (device u8) and/or host_rgb8[j]
+ * (host, ideally pinned, u8 copied D2H on the frame's stream); any array or
+ * entry may be NULL.  check != 0: synchronise and verify the tile-key
+ * capacity, re-rendering the batch after growing it if needed; check == 0:
+ * fully asynchronous (capacity learnt from earlier renders). */
+int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const gsv_camera* cam,
+                           float* const* out_rgb, uint8_t* const* out_rgb8,
+                           uint8_t* const* host_rgb8, int nstreams, int check);
+/* after unchecked batches: GSV_OK, or GSV_E_NOMEM if any frame overflowed */
+int gsv_session_check_capacity(gsv_session* s);
 /* render an fp64 SoA Gaussian set resident in HBM (render_set) */
 int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos,
                    const double* rot, const double* scl, const double* opac, const double* sh,

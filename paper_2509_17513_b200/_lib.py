@@ -54,7 +54,8 @@ class EntryInfo_t(ctypes.Structure):
 
 class RenderStats_t(ctypes.Structure):
     _fields_ = [("n_splats", ctypes.c_int64), ("n_visible", ctypes.c_int64),
-                ("n_keys", ctypes.c_int64), ("tiles_x", ctypes.c_int32), ("tiles_y", ctypes.c_int32)]
+                ("n_keys", ctypes.c_int64), ("tiles_x", ctypes.c_int32), ("tiles_y", ctypes.c_int32),
+                ("n_keys_emitted", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -69,6 +70,7 @@ _SIGS = {
     "gsv_session_create": (_I, [_I, ctypes.c_size_t, ctypes.POINTER(_P)]),
     "gsv_session_destroy": (None, [_P]),
     "gsv_session_sync": (_I, [_P]),
+    "gsv_session_check_capacity": (_I, [_P]),
     "gsv_read_info": (_I, [_P, _SZ, ctypes.POINTER(Info_t)]),
     "gsv_read_group": (_I, [_P, _SZ, _I, ctypes.POINTER(GroupInfo_t)]),
     "gsv_read_entry": (_I, [_P, _SZ, _I, _I, _I, ctypes.POINTER(EntryInfo_t)]),
@@ -82,6 +84,7 @@ _SIGS = {
     "gsv_video_frame_values": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "gsv_video_frame_codes": (_I, [_P, _I, _P]),
     "gsv_video_render": (_I, [_P, _I, ctypes.POINTER(Camera_t), _P, _P, _P]),
+    "gsv_video_render_batch": (_I, [_P, _P, _I, ctypes.POINTER(Camera_t), _P, _P, _P, _I, _I]),
     "gsv_render_soa": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P, ctypes.POINTER(Camera_t), _P, _P,
                             _P]),
     "gsv_fold_deltas": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),

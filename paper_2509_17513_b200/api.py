@@ -338,7 +338,8 @@ class DeviceVideo:
         _post(self.session)
         if stats:
             return out, {"n_splats": st.n_splats, "n_visible": st.n_visible,
-                         "n_keys": st.n_keys, "tiles": (st.tiles_x, st.tiles_y)}
+                         "n_keys": st.n_keys, "n_keys_emitted": st.n_keys_emitted,
+                         "tiles": (st.tiles_x, st.tiles_y)}
         return out
 
     def render_async(self, t: int, cam_struct, out: torch.Tensor | None,
@@ -348,6 +349,30 @@ class DeviceVideo:
         stats=True first); `check_overflow()` after a sync verifies it."""
         check(self.lib.gsv_video_render(self.handle, int(t), ctypes.byref(cam_struct), _ptr(out),
                                         _ptr(out_u8), ctypes.c_void_p(1)))
+
+    def render_batch(self, frames, cam, outs=None, outs_u8=None, host_u8=None,
+                     streams: int = 8, verify: bool = True):
+        """Render frames[j] frame-parallel on `streams` CUDA streams.  outs /
+        outs_u8: per-frame device tensors (fp32 / u8, (H, W, 3)) or None;
+        host_u8: per-frame host (pinned) u8 tensors filled by D2H copies."""
+        n = len(frames)
+        c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
+        fr = (ctypes.c_int32 * n)(*[int(t) for t in frames])
+
+        def arr(ts):
+            if ts is None:
+                return None
+            return (ctypes.c_void_p * n)(*[None if t is None else t.data_ptr() for t in ts])
+        a_out, a_u8, a_host = arr(outs), arr(outs_u8), arr(host_u8)
+        _pre(self.session)
+        check_ = 1 if verify else 0
+        rc = self.lib.gsv_video_render_batch(self.handle, fr, n, ctypes.byref(c),
+                                             ctypes.cast(a_out, ctypes.c_void_p) if a_out else None,
+                                             ctypes.cast(a_u8, ctypes.c_void_p) if a_u8 else None,
+                                             ctypes.cast(a_host, ctypes.c_void_p) if a_host else None,
+                                             int(streams), check_)
+        _lib.check(rc)
+        _post(self.session)
 
     def to_decoded_video(self) -> DecodedVideo:
         groups = []
@@ -420,7 +445,7 @@ def render_soa_tensors(tensors, sh_degree: int, cam, session: Session | None = N
     _post(s)
     if stats:
         return out, {"n_splats": st.n_splats, "n_visible": st.n_visible, "n_keys": st.n_keys,
-                     "tiles": (st.tiles_x, st.tiles_y)}
+                     "n_keys_emitted": st.n_keys_emitted, "tiles": (st.tiles_x, st.tiles_y)}
     return out
 
 

@@ -25,6 +25,16 @@ struct gsv_session {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     RenderWork work;
+    // frame-parallel rendering: independent frames on auxiliary streams, each
+    // with its own workspace, so the many small latency-bound kernels of a
+    // frame overlap with other frames' kernels
+    std::vector<cudaStream_t> aux;
+    std::vector<RenderWork*> aux_work;
+    std::vector<uint8_t*> aux_u8;  // staging for host u8 outputs
+    std::vector<size_t> aux_u8_cap;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
+    int64_t kcap_hint = 0;
 };
 
 namespace {
@@ -504,6 +514,15 @@ void gsv_session_destroy(gsv_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
+    for (size_t i = 0; i < s->aux.size(); i++) {
+        cudaStreamSynchronize(s->aux[i]);
+        work_free(s->aux_work[i]);
+        delete s->aux_work[i];
+        if (s->aux_u8[i]) cudaFree(s->aux_u8[i]);
+        cudaStreamDestroy(s->aux[i]);
+        cudaEventDestroy(s->ev_join[i]);
+    }
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     work_free(&s->work);
     if (s->own_stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -587,6 +606,83 @@ int gsv_video_render(gsv_video* v, int t, const gsv_camera* cam, float* out_rgb,
     if (rc) return rc;
     if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
     return render_planes(src, make_cam(*cam), &v->s->work, out_rgb, out_rgb8, stats, v->s->stream);
+}
+
+int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const gsv_camera* cam,
+                           float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8,
+                           int nstreams, int check) {
+    gsv_session* s = v->s;
+    if (count <= 0) return GSV_OK;
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    nstreams = std::max(1, std::min(nstreams, 32));
+    while ((int)s->aux.size() < nstreams) {
+        cudaStream_t st;
+        GSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t e;
+        GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->aux.push_back(st);
+        s->aux_work.push_back(new RenderWork());
+        s->aux_u8.push_back(nullptr);
+        s->aux_u8_cap.push_back(0);
+        s->ev_join.push_back(e);
+    }
+    if (!s->ev_fork) GSV_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    const CamDev cd = make_cam(*cam);
+    const size_t img8 = (size_t)cam->width * cam->height * 3;
+    for (int attempt = 0; attempt < 4; attempt++) {
+        const int64_t khint = std::max(s->kcap_hint, s->work.cap_k);
+        for (int i = 0; i < nstreams; i++) {
+            if (s->aux_work[i]->cap_k < khint) {
+                int rc = work_reserve(s->aux_work[i], 1, khint, 0, 0);
+                if (rc) return rc;
+            }
+            if (host_rgb8 && s->aux_u8_cap[i] < img8) {
+                if (s->aux_u8[i]) cudaFree(s->aux_u8[i]);
+                GSV_CUDA(cudaMalloc(&s->aux_u8[i], img8));
+                s->aux_u8_cap[i] = img8;
+            }
+        }
+        GSV_CUDA(cudaEventRecord(s->ev_fork, s->stream));
+        for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_fork, 0));
+        for (int j = 0; j < count; j++) {
+            const int i = j % nstreams;
+            FrameSrc src;
+            int rc = frame_src(v, frames[j], &src);
+            if (rc) return rc;
+            uint8_t* o8 = out_rgb8 ? out_rgb8[j] : nullptr;
+            const bool to_host = host_rgb8 && host_rgb8[j];
+            if (to_host) o8 = s->aux_u8[i];
+            rc = render_planes(src, cd, s->aux_work[i], out_rgb ? out_rgb[j] : nullptr, o8,
+                               reinterpret_cast<gsv_render_stats*>(1), s->aux[i]);
+            if (rc) return rc;
+            if (to_host) GSV_CUDA(cudaMemcpyAsync(host_rgb8[j], o8, img8, cudaMemcpyDeviceToHost, s->aux[i]));
+        }
+        for (int i = 0; i < nstreams; i++) {
+            GSV_CUDA(cudaEventRecord(s->ev_join[i], s->aux[i]));
+            GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join[i], 0));
+        }
+        if (!check) return GSV_OK;
+        GSV_CUDA(cudaStreamSynchronize(s->stream));
+        int64_t need = 0;
+        for (int i = 0; i < nstreams; i++) {
+            RenderWork* w = s->aux_work[i];
+            if (w->h_ctr && (int64_t)w->h_ctr[9] > w->cap_k) need = std::max(need, (int64_t)w->h_ctr[9]);
+        }
+        if (need == 0) return GSV_OK;
+        s->kcap_hint = need + need / 4 + 1024;  // grow and render the batch again
+    }
+    return fail(GSV_E_NOMEM, "tile key buffer could not be sized");
+}
+
+int gsv_session_check_capacity(gsv_session* s) {
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    for (size_t i = 0; i < s->aux.size(); i++) {
+        GSV_CUDA(cudaStreamSynchronize(s->aux[i]));
+        const RenderWork* w = s->aux_work[i];
+        if (w->h_ctr && (int64_t)w->h_ctr[9] > w->cap_k)
+            return fail(GSV_E_NOMEM, "tile key capacity exceeded in an unchecked batch");
+    }
+    return GSV_OK;
 }
 
 int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos, const double* rot,

@@ -160,8 +160,11 @@ struct RenderWork {
     // per key
     uint32_t* tkey[2] = {nullptr, nullptr};
     uint32_t* tval[2] = {nullptr, nullptr};
-    // per tile
+    // per tile / per pixel
     uint32_t* range = nullptr;               // [tiles][2]
+    uint8_t* tile_done = nullptr;            // saturated tiles
+    float4* state = nullptr;                 // per pixel (C.rgb, T) carried across rounds
+    int64_t cap_pix = 0;
     // radix / scan scratch
     uint32_t* hist = nullptr;
     int64_t hist_cap = 0;
@@ -171,7 +174,7 @@ struct RenderWork {
     unsigned long long* h_ctr = nullptr;     // pinned mirror
 };
 
-int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles);
+int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix);
 void work_free(RenderWork* w);
 
 // byte copy job (RAW planes of range-coded runs -> aligned storage)
@@ -193,6 +196,13 @@ void launch_crc(const RunDesc* runs, const PlaneRef* planes, int nplanes,
 void launch_dequant_frame(const FrameSrc& src, double* pos, double* rot, double* scl,
                           double* opac, double* sh, cudaStream_t s);
 void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
+
+// composite.cu
+void launch_state_init(float4* state, uint8_t* tile_done, size_t npix, int ntiles, cudaStream_t s);
+void launch_composite_round(const uint32_t* ranks, const uint32_t* range, const SplatRec* recs,
+                            float4* state, uint8_t* tile_done, const CamDev& cam, cudaStream_t s);
+void launch_finalize(const float4* state, const CamDev& cam, float* out_rgb, uint8_t* out_rgb8,
+                     cudaStream_t s);
 
 // render.cu: full per-frame pipeline
 int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,

@@ -25,11 +25,10 @@ namespace gsv {
 void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
 void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* dbg_rect,
                         double* dbg_depth, cudaStream_t s);
-void launch_composite(const uint32_t* ranks, const uint32_t* range, const SplatRec* recs,
-                      const CamDev& cam, float* out_rgb, uint8_t* out_rgb8, cudaStream_t s);
 
 enum { C_NVIS = 0, C_NKEYS = 1, C_DMIN = 2, C_DMAX = 3, C_OVF = 4, C_N = 5, C_KCLAMP = 6,
-       C_NPASS = 8 /* int */ };
+       C_RN = 7, C_NPASS = 8 /* int */, C_MAXK = 9 /* sticky across frames */, C_TOTK = 10,
+       C_EMITK = 11 };
 
 CamDev make_cam(const gsv_camera& c) {
     CamDev d;
@@ -60,7 +59,9 @@ __global__ void reset_ctr_kernel(unsigned long long* ctr, long long n) {
     ctr[C_OVF] = 0;
     ctr[C_N] = (unsigned long long)n;
     ctr[C_KCLAMP] = 0;
-    ctr[7] = 0;
+    ctr[C_RN] = 0;
+    ctr[C_TOTK] = 0;
+    ctr[C_EMITK] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[0] = 0;
 }
 
@@ -87,42 +88,73 @@ __device__ __forceinline__ uint32_t rec_tile_count(const SplatRec& r) {
     return ((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1);
 }
 
-// rank r -> record in rank order + its tile count
-__global__ void emit_prep(const SplatRec* __restrict__ rec,
-                          SplatRec* __restrict__ rec_sorted, uint32_t* __restrict__ cnt,
-                          const unsigned long long* __restrict__ ctr, uint32_t* didx0,
-                          uint32_t* didx1) {
+// rank r -> record in rank order
+// (also totals the (tile, splat) overlaps: the tile-key count without early out)
+__global__ void gather_sorted(const SplatRec* __restrict__ rec, SplatRec* __restrict__ rec_sorted,
+                              unsigned long long* __restrict__ ctr, const uint32_t* __restrict__ didx0,
+                              const uint32_t* __restrict__ didx1) {
     const uint32_t nvis = (uint32_t)ctr[C_NVIS];
     const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
     const uint32_t* idx = (np & 1) ? didx1 : didx0;
+    unsigned long long tot = 0;
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nvis; r += gridDim.x * blockDim.x) {
         const SplatRec s = rec[idx[r]];
         rec_sorted[r] = s;
-        cnt[r] = rec_tile_count(s);
+        tot += rec_tile_count(s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(ctr + C_TOTK, tot);
+}
+
+// Round [a, b) of the depth ranks: number of not-yet-saturated tiles each
+// splat overlaps.  Also publishes the round's splat count.
+__global__ void round_count(const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr,
+                            uint32_t a, uint32_t b, const uint8_t* __restrict__ tile_done,
+                            uint32_t* __restrict__ cnt, int ntx) {
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const uint32_t hi = b < nvis ? b : nvis;
+    const uint32_t m = hi > a ? hi - a : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr[C_RN] = m;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const SplatRec s = rec_sorted[a + i];
+        const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
+        const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
+        uint32_t c = 0;
+        for (uint32_t ty = y0; ty <= y1; ty++)
+            for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] ? 0u : 1u;
+        cnt[i] = c;
     }
 }
 
-// scatter (tile, rank) keys in rank order
-__global__ void emit_keys(const SplatRec* __restrict__ rec_sorted, const uint32_t* __restrict__ off,
-                          unsigned long long* __restrict__ ctr, uint32_t* __restrict__ tkey,
-                          uint32_t* __restrict__ tval, uint64_t cap, int ntx) {
-    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+// scatter (tile, rank) keys of the round in rank order
+__global__ void round_emit(const SplatRec* __restrict__ rec_sorted, const uint32_t* __restrict__ off,
+                           unsigned long long* __restrict__ ctr, uint32_t a,
+                           const uint8_t* __restrict__ tile_done, uint32_t* __restrict__ tkey,
+                           uint32_t* __restrict__ tval, uint64_t cap, int ntx) {
+    const uint32_t m = (uint32_t)ctr[C_RN];
     const uint64_t K = ctr[C_NKEYS];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctr[C_KCLAMP] = K < cap ? K : cap;
         if (K > cap) ctr[C_OVF] = K;
+        atomicMax(ctr + C_MAXK, (unsigned long long)K);
+        ctr[C_EMITK] += K;
     }
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nvis; r += gridDim.x * blockDim.x) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const uint32_t r = a + i;
         const SplatRec s = rec_sorted[r];
         const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
         const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
-        uint64_t o = off[r];
+        uint64_t o = off[i];
         for (uint32_t ty = y0; ty <= y1; ty++)
-            for (uint32_t tx = x0; tx <= x1; tx++, o++) {
+            for (uint32_t tx = x0; tx <= x1; tx++) {
+                const uint32_t t = ty * (uint32_t)ntx + tx;
+                if (tile_done[t]) continue;
                 if (o < cap) {
-                    tkey[o] = ty * (uint32_t)ntx + tx;
+                    tkey[o] = t;
                     tval[o] = r;
                 }
+                o++;
             }
     }
 }
@@ -153,13 +185,15 @@ void work_free(RenderWork* w) {
     free_ptr(w->rec_sorted);
     free_ptr(w->cnt);
     free_ptr(w->range);
+    free_ptr(w->state);
+    free_ptr(w->tile_done);
     free_ptr(w->hist);
     free_ptr(w->ctr);
     if (w->h_ctr) cudaFreeHost(w->h_ctr);
     *w = RenderWork();
 }
 
-int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles) {
+int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
     if (!w->ctr) {
         GSV_CUDA(cudaMalloc(&w->ctr, 16 * sizeof(unsigned long long)));
         GSV_CUDA(cudaMallocHost(&w->h_ctr, 16 * sizeof(unsigned long long)));
@@ -194,8 +228,15 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles) {
     }
     if (tiles > w->cap_tiles) {
         free_ptr(w->range);
+        free_ptr(w->tile_done);
         GSV_CUDA(cudaMalloc(&w->range, (size_t)tiles * 2 * sizeof(uint32_t)));
+        GSV_CUDA(cudaMalloc(&w->tile_done, (size_t)tiles));
         w->cap_tiles = tiles;
+    }
+    if (npix > w->cap_pix) {
+        free_ptr(w->state);
+        GSV_CUDA(cudaMalloc(&w->state, (size_t)npix * sizeof(float4)));
+        w->cap_pix = npix;
     }
     const int64_t hw = std::max(radix_hist_words(std::max(w->cap_n, w->cap_k)),
                                 scan_bsum_words(w->cap_n)) + 512;
@@ -213,14 +254,30 @@ static int tile_passes(int ntiles) {
     return std::max(1, (bits + 7) / 8);
 }
 
+// Depth-rank rounds: [0, 32k), [32k, 128k), [128k, 512k), ... Tiles saturate
+// within the first few tens of thousands of ranks (~97
+// evaluations per covered pixel), so later rounds only emit keys for the
+// few tiles that are still open.
+static void round_bounds(int64_t n, std::vector<uint32_t>* b) {
+    b->clear();
+    uint64_t x = 0, step = 32768;
+    while ((int64_t)x < n) {
+        b->push_back((uint32_t)x);
+        x += step;
+        step *= 4;
+    }
+    b->push_back((uint32_t)std::max<int64_t>(n, 0));
+}
+
 // Enqueue one frame.  `project` enqueues the projection kernel into w.
 template <class Proj>
 static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj project,
                           float* out_rgb, uint8_t* out_rgb8, cudaStream_t s) {
     const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
     const int ntiles = ntx * nty;
+    const int64_t npix = (int64_t)cam.width * cam.height;
     if (cam.width > 65535 || cam.height > 65535) return fail(GSV_E_INVALID_INPUT, "image too large");
-    int rc = work_reserve(w, n, std::max<int64_t>(w->cap_k, 16 * n), ntiles);
+    int rc = work_reserve(w, n, std::max<int64_t>(w->cap_k, 4 * n), ntiles, npix);
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
@@ -236,22 +293,33 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         count_launch(1 + 3 * 8);
     }
     prof_mark(ST_EMIT, s);
-    const unsigned g = 148 * 8;
-    emit_prep<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, w->cnt, ctr, w->didx[0], w->didx[1]);
-    exclusive_scan(w->cnt, ctr + C_NVIS, w->cap_n, w->hist, ctr + C_NKEYS, s);
-    emit_keys<<<g, 256, 0, s>>>(w->rec_sorted, w->cnt, ctr, w->tkey[0], w->tval[0],
-                                (uint64_t)w->cap_k, ntx);
-    count_launch(5);
-    prof_mark(ST_TSORT, s);
+    const unsigned g = 148 * 4;
+    gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
+    launch_state_init(w->state, w->tile_done, (size_t)npix, ntiles, s);
+    count_launch(2);
+    std::vector<uint32_t> bounds;
+    round_bounds(n, &bounds);
     const int tp = tile_passes(ntiles);
-    radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, w->hist, digit_total, s);
-    count_launch(3 * tp);
-    prof_mark(ST_RANGES, s);
-    cudaMemsetAsync(w->range, 0, (size_t)ntiles * 2 * sizeof(uint32_t), s);
-    tile_ranges<<<g, 256, 0, s>>>(w->tkey[tp & 1], ctr, w->range);
-    count_launch(1);
-    prof_mark(ST_COMPOSITE, s);
-    launch_composite(w->tval[tp & 1], w->range, w->rec_sorted, cam, out_rgb, out_rgb8, s);
+    for (size_t j = 0; j + 1 < bounds.size(); j++) {
+        const uint32_t a = bounds[j], b = bounds[j + 1];
+        prof_mark(ST_EMIT, s);
+        round_count<<<g, 256, 0, s>>>(w->rec_sorted, ctr, a, b, w->tile_done, w->cnt, ntx);
+        exclusive_scan(w->cnt, ctr + C_RN, (int64_t)(b - a), w->hist, ctr + C_NKEYS, s);
+        round_emit<<<g, 256, 0, s>>>(w->rec_sorted, w->cnt, ctr, a, w->tile_done, w->tkey[0], w->tval[0],
+                                     (uint64_t)w->cap_k, ntx);
+        count_launch(5);
+        prof_mark(ST_TSORT, s);
+        radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, w->hist, digit_total, s);
+        count_launch(3 * tp);
+        prof_mark(ST_RANGES, s);
+        cudaMemsetAsync(w->range, 0, (size_t)ntiles * 2 * sizeof(uint32_t), s);
+        tile_ranges<<<g, 256, 0, s>>>(w->tkey[tp & 1], ctr, w->range);
+        count_launch(1);
+        prof_mark(ST_COMPOSITE, s);
+        launch_composite_round(w->tval[tp & 1], w->range, w->rec_sorted, w->state, w->tile_done, cam, s);
+        count_launch(1);
+    }
+    launch_finalize(w->state, cam, out_rgb, out_rgb8, s);
     count_launch(1);
     prof_mark(ST_COUNT, s);
     cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
@@ -263,22 +331,23 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
 template <class Proj>
 static int render_checked(int64_t n, const CamDev& cam, RenderWork* w, Proj project, float* out_rgb,
                           uint8_t* out_rgb8, gsv_render_stats* st, cudaStream_t s) {
-    for (int attempt = 0; attempt < 4; attempt++) {
+    for (int attempt = 0; attempt < 6; attempt++) {
         int rc = render_enqueue(n, cam, w, project, out_rgb, out_rgb8, s);
         if (rc) return rc;
         GSV_CUDA(cudaStreamSynchronize(s));
-        const unsigned long long K = w->h_ctr[C_NKEYS];
-        if (w->h_ctr[C_OVF] == 0) {
+        const unsigned long long K = w->h_ctr[C_MAXK];
+        if (K <= (unsigned long long)w->cap_k) {
             if (st) {
                 st->n_splats = n;
                 st->n_visible = (int64_t)w->h_ctr[C_NVIS];
-                st->n_keys = (int64_t)K;
+                st->n_keys = (int64_t)w->h_ctr[C_TOTK];
+                st->n_keys_emitted = (int64_t)w->h_ctr[C_EMITK];
                 st->tiles_x = (cam.width + kTile - 1) / kTile;
                 st->tiles_y = (cam.height + kTile - 1) / kTile;
             }
             return GSV_OK;
         }
-        rc = work_reserve(w, n, (int64_t)(K + K / 4 + 1024), 0);
+        rc = work_reserve(w, n, (int64_t)(K + K / 4 + 1024), 0, 0);
         if (rc) return rc;
     }
     return fail(GSV_E_NOMEM, "tile key buffer could not be sized");
@@ -318,7 +387,7 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s) {
     const int64_t n = src.n;
-    int rc = work_reserve(w, n, w->cap_k, 1);
+    int rc = work_reserve(w, n, w->cap_k, 1, 0);
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
