@@ -680,7 +680,9 @@ int gsv_session_check_capacity(gsv_session* s) {
         GSV_CUDA(cudaStreamSynchronize(s->aux[i]));
         const RenderWork* w = s->aux_work[i];
         if (w->h_ctr && (int64_t)w->h_ctr[9] > w->cap_k)
-            return fail(GSV_E_NOMEM, "tile key capacity exceeded in an unchecked batch");
+            return fail(GSV_E_NOMEM, "tile key capacity exceeded in an unchecked batch (stream " +
+                                         std::to_string(i) + ": " + std::to_string(w->h_ctr[9]) + " > " +
+                                         std::to_string(w->cap_k) + ")");
     }
     return GSV_OK;
 }

@@ -1,35 +1,55 @@
 // Front-to-back alpha compositing over 16x16 tiles (render.py:301-356),
 // resumable across depth-rank rounds.
 //
-// One CTA per tile, one thread per pixel.  A round hands every tile the
+// One CTA per tile, one thread per pixel, each warp an 8x4 pixel block.  A
+// round hands every tile the
 // records of its splats whose depth ranks fall in the round's range, in rank
 // order; the pixel's (C, T) state is loaded from and stored back to
 // `state`, so running the rounds in order is the same per-pixel loop as the
 // reference's (render.py:307-332): integer rect clip, T < 1e-4 skip, power
 // clamp, 0.99 alpha cap, alpha <= 0 skip, fp32 accumulation in a fixed
 // order (deterministic).  Records are staged through shared memory 256 at a
-// time; each warp skips records whose rect misses its two pixel rows, and
-// the CTA stops as soon as every pixel has saturated, marking the tile done
-// so later rounds emit no keys for it.
+// time; each warp ballots 32 records at a time against its block's bounds
+// and walks only the hits, leaves as soon as its 32 pixels are saturated,
+// and the CTA stops once every pixel has saturated, marking the tile done so
+// later rounds emit no keys for it.
 #include <stdint.h>
 
 #include "gsv_internal.h"
 
 namespace gsv {
 
+// first index in the tile-sorted keys with key >= t
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ k, uint32_t n, uint32_t t) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(k + mid) < t) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(256) composite_round_kernel(
-    const uint32_t* __restrict__ ranks, const uint32_t* __restrict__ range,
-    const SplatRec* __restrict__ recs, float4* __restrict__ state, uint8_t* __restrict__ tile_done,
-    int width, int height, int ntx) {
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
+    const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
+    float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx) {
     __shared__ float4 s_a[256], s_b[256];
     __shared__ uint4 s_c[256];
+    __shared__ uint32_t s_range[2];
     const int tile = blockIdx.x;
-    const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
+    if (threadIdx.x < 2) {  // this tile's [start, end) in the tile-sorted keys
+        const uint32_t K = (uint32_t)*nkeys;
+        s_range[threadIdx.x] = lower_bound_u32(keys, K, (uint32_t)tile + threadIdx.x);
+    }
+    __syncthreads();
+    const uint32_t start = s_range[0], end = s_range[1];
     if (start >= end) return;
     const int tx = tile % ntx, ty = tile / ntx;
-    const int px = tx * kTile + (threadIdx.x & 15);
-    const int py = ty * kTile + (threadIdx.x >> 4);
-    const int wy0 = ty * kTile + 2 * (threadIdx.x >> 5);  // this warp's two pixel rows
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp w owns an 8x4 pixel block of the 16x16 tile
+    const int bx0 = tx * kTile + (warp & 1) * 8, by0 = ty * kTile + (warp >> 1) * 4;
+    const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
     const bool inside = px < width && py < height;
     const size_t pix = (size_t)py * width + px;
     float4 st = inside ? state[pix] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -46,30 +66,43 @@ __global__ void __launch_bounds__(256) composite_round_kernel(
         }
         __syncthreads();
         const int cnt = (int)min(256u, end - base);
-        if (!__all_sync(0xffffffffu, done)) {
-            for (int q = 0; q < cnt; q++) {
-                const uint4 c = s_c[q];  // op bits, rx, ry, pad
-                const int y0 = (int)(c.z & 0xFFFFu), y1 = (int)(c.z >> 16);
-                if (wy0 + 1 < y0 || wy0 >= y1) continue;  // warp-uniform row test
+        for (int g = 0; g < cnt; g += 32) {
+            if (__all_sync(0xffffffffu, done)) break;
+            // which of the next 32 records touch this warp's 8x4 block?
+            bool hit = false;
+            if (g + lane < cnt) {
+                const uint4 c = s_c[g + lane];
                 const int x0 = (int)(c.y & 0xFFFFu), x1 = (int)(c.y >> 16);
-                if (done || px < x0 || px >= x1 || py < y0 || py >= y1) continue;
+                const int y0 = (int)(c.z & 0xFFFFu), y1 = (int)(c.z >> 16);
+                hit = x0 < bx0 + 8 && x1 > bx0 && y0 < by0 + 4 && y1 > by0;
+            }
+            uint32_t mask = __ballot_sync(0xffffffffu, hit);
+            while (mask) {
+                const int q = g + __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (done) continue;
+                const uint4 c = s_c[q];  // op bits, rx, ry, pad
+                const int ix = px - (int)(c.y & 0xFFFFu), iy = py - (int)(c.z & 0xFFFFu);
+                if ((unsigned)ix >= (c.y >> 16) - (c.y & 0xFFFFu) ||
+                    (unsigned)iy >= (c.z >> 16) - (c.z & 0xFFFFu))
+                    continue;  // outside the splat's integer rect (render.py:313-315)
                 if (T < 1e-4f) {
                     done = true;
                     continue;
                 }
                 const float4 a = s_a[q];  // ox, oy, ca, cb
                 const float4 b = s_b[q];  // cc, r, g, b
-                const float dx = (float)(px - x0) - a.x;
-                const float dy = (float)(py - y0) - a.y;
-                float power = -0.5f * (a.z * dx * dx + 2.0f * a.w * dx * dy + b.x * dy * dy);
-                power = power > 0.0f ? 0.0f : power;
-                float alpha = __uint_as_float(c.x) * __expf(power);
-                alpha = alpha > 0.99f ? 0.99f : alpha;
+                const float dx = (float)ix - a.x;
+                const float dy = (float)iy - a.y;
+                const float pw = fminf(fmaf(fmaf(a.z, dx, a.w * dy), dx, b.x * dy * dy), 0.0f);
+                float e;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw));
+                const float alpha = fminf(__uint_as_float(c.x) * e, 0.99f);
                 if (alpha <= 0.0f) continue;
                 const float w = T * alpha;
-                c0 += w * b.y;
-                c1 += w * b.z;
-                c2 += w * b.w;
+                c0 = fmaf(w, b.y, c0);
+                c1 = fmaf(w, b.z, c1);
+                c2 = fmaf(w, b.w, c2);
                 T = T * (1.0f - alpha);
             }
         }
@@ -106,11 +139,12 @@ void launch_state_init(float4* state, uint8_t* tile_done, size_t npix, int ntile
     state_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(state, tile_done, npix, ntiles);
 }
 
-void launch_composite_round(const uint32_t* ranks, const uint32_t* range, const SplatRec* recs,
-                            float4* state, uint8_t* tile_done, const CamDev& cam, cudaStream_t s) {
+void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
+                            const unsigned long long* nkeys, const SplatRec* recs, float4* state,
+                            uint8_t* tile_done, const CamDev& cam, cudaStream_t s) {
     const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
-    composite_round_kernel<<<ntx * nty, 256, 0, s>>>(ranks, range, recs, state, tile_done, cam.width,
-                                                     cam.height, ntx);
+    composite_round_kernel<<<ntx * nty, 256, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done,
+                                                     cam.width, cam.height, ntx);
 }
 
 void launch_finalize(const float4* state, const CamDev& cam, float* out_rgb, uint8_t* out_rgb8,

@@ -135,7 +135,9 @@ struct CamDev {
 };
 
 // 48-byte splat record consumed by the compositor (all fp32):
-//   ox, oy : mean - rect origin (px)       ca, cb, cc : conic inverse (render.py:346-349)
+//   ox, oy : mean - rect origin (px)
+//   ca, cb, cc : -log2(e)/2 * (a, 2b, c) of the conic inverse (render.py:346-349),
+//                so alpha = op * 2^(ca dx^2 + cb dx dy + cc dy^2)
 //   r, g, b: SH colour in [0,1]             op : opacity
 //   rx, ry : x0 | x1 << 16, y0 | y1 << 16   (u16 each)
 struct __align__(16) SplatRec {
@@ -165,6 +167,10 @@ struct RenderWork {
     uint8_t* tile_done = nullptr;            // saturated tiles
     float4* state = nullptr;                 // per pixel (C.rgb, T) carried across rounds
     int64_t cap_pix = 0;
+    // decoupled look-back scan state of the fused key emission
+    unsigned long long* status = nullptr;
+    unsigned int* ticket = nullptr;
+    uint32_t epoch = 0;
     // radix / scan scratch
     uint32_t* hist = nullptr;
     int64_t hist_cap = 0;
@@ -199,8 +205,9 @@ void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
 
 // composite.cu
 void launch_state_init(float4* state, uint8_t* tile_done, size_t npix, int ntiles, cudaStream_t s);
-void launch_composite_round(const uint32_t* ranks, const uint32_t* range, const SplatRec* recs,
-                            float4* state, uint8_t* tile_done, const CamDev& cam, cudaStream_t s);
+void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
+                            const unsigned long long* nkeys, const SplatRec* recs, float4* state,
+                            uint8_t* tile_done, const CamDev& cam, cudaStream_t s);
 void launch_finalize(const float4* state, const CamDev& cam, float* out_rgb, uint8_t* out_rgb8,
                      cudaStream_t s);
 

@@ -31,9 +31,31 @@ __device__ __forceinline__ uint32_t load_sample_p(const uint8_t* p, uint32_t j, 
            ((uint32_t)__ldg(q + 3) << 24);
 }
 
+// code / (2^bits - 1) for 8- and 16-bit codes, tabulated: the quotient is the
+// correctly rounded fp64 division, so rmin + q * (rmax - rmin) stays
+// bit-identical to dequantize_codes (quantize.py:114-117) without an fp64
+// division per channel.
+__device__ double g_q8[256];
+__device__ double g_q16[65536];
+
 __device__ __forceinline__ double dequant_p(uint32_t code, const SlotDesc& sd) {
-    const double top = sd.dir_bits >= 32 ? 4294967295.0 : (double)((1ull << sd.dir_bits) - 1ull);
-    return __dadd_rn(sd.rmin, __dmul_rn(__ddiv_rn((double)code, top), __dsub_rn(sd.rmax, sd.rmin)));
+    double q;
+    if (sd.dir_bits == 8 && code < 256u) q = __ldg(g_q8 + code);
+    else if (sd.dir_bits == 16 && code < 65536u) q = __ldg(g_q16 + code);
+    else q = __ddiv_rn((double)code, sd.dir_bits >= 32 ? 4294967295.0
+                                                        : (double)((1ull << sd.dir_bits) - 1ull));
+    return __dadd_rn(sd.rmin, __dmul_rn(q, __dsub_rn(sd.rmax, sd.rmin)));
+}
+
+static void init_quotient_tables() {
+    static bool done = false;
+    if (done) return;
+    static double t8[256], t16[65536];
+    for (int i = 0; i < 256; i++) t8[i] = (double)i / 255.0;
+    for (int i = 0; i < 65536; i++) t16[i] = (double)i / 65535.0;
+    cudaMemcpyToSymbol(g_q8, t8, sizeof t8);
+    cudaMemcpyToSymbol(g_q16, t16, sizeof t16);
+    done = true;
 }
 
 // Splat attributes in fp64 registers.
@@ -47,14 +69,16 @@ struct SplatIn {
 struct PlaneLoader {
     FrameSrc src;
     __device__ __forceinline__ int64_t count() const { return src.layer_off[src.nlayers]; }
-    template <int DEG>
+    // slots [S0, S1): geometry (0..10) first, SH (11..) only for survivors,
+    // which keeps the SH registers out of the projection's live range
+    template <int DEG, int S0, int S1>
     __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a) const {
         int l = 0;
         while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
         const uint32_t j = i - src.layer_off[l];
         const SlotDesc* sd = src.slots + (size_t)l * src.nslots;
 #pragma unroll
-        for (int s = 0; s < 11 + SplatIn<DEG>::SHD; s++) {
+        for (int s = S0; s < S1; s++) {
             const SlotDesc d = sd[s];
             const double v = dequant_p(load_sample_p(src.planes[d.plane_base + src.frame].samples, j, d.bits), d);
             if (s < 3) a.p[s] = v;
@@ -69,18 +93,21 @@ struct PlaneLoader {
 struct SoaLoader {
     SoaSrc src;
     __device__ __forceinline__ int64_t count() const { return src.n; }
-    template <int DEG>
+    template <int DEG, int S0, int S1>
     __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a) const {
         constexpr int shdim = SplatIn<DEG>::SHD;
+        if constexpr (S0 == 0) {
 #pragma unroll
-        for (int k = 0; k < 3; k++) a.p[k] = src.pos[3 * (size_t)i + k];
+            for (int k = 0; k < 3; k++) a.p[k] = src.pos[3 * (size_t)i + k];
 #pragma unroll
-        for (int k = 0; k < 4; k++) a.q[k] = src.rot[4 * (size_t)i + k];
+            for (int k = 0; k < 4; k++) a.q[k] = src.rot[4 * (size_t)i + k];
 #pragma unroll
-        for (int k = 0; k < 3; k++) a.s[k] = src.scl[3 * (size_t)i + k];
-        a.o = src.opac[i];
+            for (int k = 0; k < 3; k++) a.s[k] = src.scl[3 * (size_t)i + k];
+            a.o = src.opac[i];
+        } else {
 #pragma unroll
-        for (int k = 0; k < shdim; k++) a.sh[k] = src.sh[(size_t)shdim * i + k];
+            for (int k = 0; k < shdim; k++) a.sh[k] = src.sh[(size_t)shdim * i + k];
+        }
     }
 };
 
@@ -237,21 +264,25 @@ __global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
     uint64_t key = ~0ull;
     if (i < n) {
         SplatIn<DEG> a;
-        ld.load((uint32_t)i, a);
+        ld.template load<DEG, 0, 11>((uint32_t)i, a);
         const ProjOut o = project_one(a, cam);
         alive = o.alive;
         if (dbg_depth) dbg_depth[i] = o.depth;
         if (alive) {
             key = (uint64_t)__double_as_longlong(o.depth);
+            ld.template load<DEG, 11, 11 + SplatIn<DEG>::SHD>((uint32_t)i, a);
             double rgb[3];
             sh_color(a, cam, rgb);
             const double det = o.cov[0] * o.cov[3] - o.cov[1] * o.cov[1];
             SplatRec r;
             r.ox = (float)(o.u - o.x0);
             r.oy = (float)(o.v - o.y0);
-            r.ca = (float)(o.cov[3] / det);
-            r.cb = (float)(-o.cov[1] / det);
-            r.cc = (float)(o.cov[0] / det);
+            // conic (render.py:346-349) folded into the base-2 exponent the
+            // compositor evaluates: log2(e) * -0.5 * (a dx^2 + 2 b dx dy + c dy^2)
+            const double l2e = 1.4426950408889634;
+            r.ca = (float)(-0.5 * l2e * (o.cov[3] / det));
+            r.cb = (float)(-l2e * (-o.cov[1] / det));
+            r.cc = (float)(-0.5 * l2e * (o.cov[0] / det));
             r.r = (float)rgb[0];
             r.g = (float)rgb[1];
             r.b = (float)rgb[2];
@@ -303,6 +334,7 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
 }
 
 void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s) {
+    init_quotient_tables();
     launch_project(PlaneLoader{src}, (int64_t)src.layer_off[src.nlayers], cam, src.sh_degree, w,
                    nullptr, nullptr, s);
 }

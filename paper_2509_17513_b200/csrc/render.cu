@@ -27,8 +27,8 @@ void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int
                         double* dbg_depth, cudaStream_t s);
 
 enum { C_NVIS = 0, C_NKEYS = 1, C_DMIN = 2, C_DMAX = 3, C_OVF = 4, C_N = 5, C_KCLAMP = 6,
-       C_RN = 7, C_NPASS = 8 /* int */, C_MAXK = 9 /* sticky across frames */, C_TOTK = 10,
-       C_EMITK = 11 };
+       C_RN = 7, C_NPASS = 8 /* int pair: passes, key shift */, C_MAXK = 9 /* sticky */,
+       C_TOTK = 10, C_EMITK = 11 };
 
 CamDev make_cam(const gsv_camera& c) {
     CamDev d;
@@ -63,23 +63,67 @@ __global__ void reset_ctr_kernel(unsigned long long* ctr, long long n) {
     ctr[C_TOTK] = 0;
     ctr[C_EMITK] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[0] = 0;
+    reinterpret_cast<int*>(ctr + C_NPASS)[1] = 0;
 }
 
-// Rebase survivor depth bits to [0, range]; culled splats get range + 1.
-// Passes needed = bytes spanned by range + 1.
-__global__ void depth_key_prep(uint64_t* __restrict__ key, unsigned long long* __restrict__ ctr) {
+// Rebase survivor depth bits to [0, range]; culled splats get range + 1 (so
+// they sort last).  The radix sort runs on the top 32 significant bits of
+// that key (key32); full[] keeps the 64-bit key by splat index for the
+// fix-up of key32 ties.  Passes = bytes spanned by key32.
+__global__ void depth_key_prep(uint64_t* __restrict__ full, uint32_t* __restrict__ key32,
+                               unsigned long long* __restrict__ ctr) {
     const uint64_t n = ctr[C_N];
     const uint64_t nvis = ctr[C_NVIS];
     const uint64_t lo = ctr[C_DMIN], hi = ctr[C_DMAX];
     const uint64_t dead = nvis ? (hi - lo) + 1 : 0;
+    const int bits = dead ? 64 - __clzll((long long)dead) : 0;
+    const int shift = bits > 32 ? bits - 32 : 0;
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
-        int bits = dead ? 64 - __clzll((long long)dead) : 0;
-        reinterpret_cast<int*>(ctr + C_NPASS)[0] = (nvis == 0 || nvis == n && hi == lo) ? 0 : (bits + 7) / 8;
+        const int kb = bits - shift;
+        reinterpret_cast<int*>(ctr + C_NPASS)[0] = (nvis == 0 || (nvis == n && hi == lo)) ? 0 : (kb + 7) / 8;
+        reinterpret_cast<int*>(ctr + C_NPASS)[1] = shift;
     }
     if (i < n) {
-        const uint64_t k = key[i];
-        key[i] = (k == ~0ull) ? dead : k - lo;
+        const uint64_t k = full[i];
+        const uint64_t r = (k == ~0ull) ? dead : k - lo;
+        full[i] = r;
+        key32[i] = (uint32_t)(r >> shift);
+    }
+}
+
+// Stable order among equal key32 values by the full key: one thread per run
+// of equal key32 (insertion sort, stable).  Runs of distinct full keys need
+// depth differences below 2^-32 of the depth range, so they are short.
+__global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t* __restrict__ k1,
+                                uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
+                                const uint64_t* __restrict__ full, const unsigned long long* __restrict__ ctr) {
+    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
+    const int shift = reinterpret_cast<const int*>(ctr + C_NPASS)[1];
+    if (shift == 0 || np == 0) return;
+    const uint32_t n = (uint32_t)ctr[C_N];
+    const uint32_t* key = (np & 1) ? k1 : k0;
+    uint32_t* idx = (np & 1) ? i1 : i0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t k = key[r];
+        if (r > 0 && key[r - 1] == k) continue;
+        uint32_t e = r + 1;
+        while (e < n && key[e] == k) e++;
+        if (e - r < 2) continue;
+        const uint64_t f0 = full[idx[r]];
+        bool same = true;
+        for (uint32_t q = r + 1; q < e && same; q++) same = full[idx[q]] == f0;
+        if (same) continue;
+        for (uint32_t q = r + 1; q < e; q++) {
+            const uint32_t v = idx[q];
+            const uint64_t fv = full[v];
+            uint32_t p = q;
+            while (p > r && full[idx[p - 1]] > fv) {
+                idx[p] = idx[p - 1];
+                p--;
+            }
+            idx[p] = v;
+        }
     }
 }
 
@@ -107,45 +151,116 @@ __global__ void gather_sorted(const SplatRec* __restrict__ rec, SplatRec* __rest
     if ((threadIdx.x & 31) == 0 && tot) atomicAdd(ctr + C_TOTK, tot);
 }
 
-// Round [a, b) of the depth ranks: number of not-yet-saturated tiles each
-// splat overlaps.  Also publishes the round's splat count.
-__global__ void round_count(const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr,
-                            uint32_t a, uint32_t b, const uint8_t* __restrict__ tile_done,
-                            uint32_t* __restrict__ cnt, int ntx) {
+// Round [a, b) of the depth ranks: count the not-yet-saturated tiles each
+// splat overlaps, turn the counts into offsets with a single-pass
+// decoupled-look-back scan across CTAs (ticketed CTA order, epoch-tagged
+// status words so nothing needs resetting between uses), and scatter the
+// (tile, rank) keys in rank order -- one launch instead of count + scan +
+// emit.
+constexpr int kEmitThreads = 256, kEmitPer = 1, kEmitTile = kEmitThreads * kEmitPer;
+
+__device__ __forceinline__ unsigned long long st_pack(uint32_t epoch, uint32_t flag, unsigned long long v) {
+    return ((unsigned long long)(epoch & 0xFFFFFFu) << 40) | ((unsigned long long)flag << 38) | v;
+}
+
+__global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
+    const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
+    const uint8_t* __restrict__ tile_done, uint32_t* __restrict__ tkey, uint32_t* __restrict__ tval,
+    uint64_t cap, int ntx, unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
+    uint32_t epoch) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_prefix;
+    __shared__ uint32_t s_wsum[kEmitThreads / 32];
+    if (threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(ticket, 1u);
+        if (t == gridDim.x - 1) *ticket = 0;  // every CTA has its ticket: reset for the next use
+        s_tile = t;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
     const uint32_t nvis = (uint32_t)ctr[C_NVIS];
     const uint32_t hi = b < nvis ? b : nvis;
     const uint32_t m = hi > a ? hi - a : 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr[C_RN] = m;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        const SplatRec s = rec_sorted[a + i];
-        const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
-        const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
-        uint32_t c = 0;
-        for (uint32_t ty = y0; ty <= y1; ty++)
-            for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] ? 0u : 1u;
-        cnt[i] = c;
+    const uint32_t nt = (m + kEmitTile - 1) / kEmitTile;
+    if (tile >= nt) {
+        if (tile == 0 && threadIdx.x == 0) {  // empty round
+            ctr[C_NKEYS] = 0;
+            ctr[C_KCLAMP] = 0;
+        }
+        return;
     }
-}
-
-// scatter (tile, rank) keys of the round in rank order
-__global__ void round_emit(const SplatRec* __restrict__ rec_sorted, const uint32_t* __restrict__ off,
-                           unsigned long long* __restrict__ ctr, uint32_t a,
-                           const uint8_t* __restrict__ tile_done, uint32_t* __restrict__ tkey,
-                           uint32_t* __restrict__ tval, uint64_t cap, int ntx) {
-    const uint32_t m = (uint32_t)ctr[C_RN];
-    const uint64_t K = ctr[C_NKEYS];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctr[C_KCLAMP] = K < cap ? K : cap;
-        if (K > cap) ctr[C_OVF] = K;
-        atomicMax(ctr + C_MAXK, (unsigned long long)K);
-        ctr[C_EMITK] += K;
+    const uint32_t base = tile * kEmitTile + threadIdx.x * kEmitPer;
+    uint32_t cnt[kEmitPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kEmitPer; k++) {
+        cnt[k] = 0;
+        if (base + k < m) {
+            const SplatRec s = rec_sorted[a + base + k];
+            const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
+            const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
+            uint32_t c = 0;
+            for (uint32_t ty = y0; ty <= y1; ty++)
+                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] ? 0u : 1u;
+            cnt[k] = c;
+        }
+        sum += cnt[k];
     }
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        const uint32_t r = a + i;
+    // block exclusive scan of the per-thread sums
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t wb = 0, total = 0;
+    for (int w = 0; w < kEmitThreads / 32; w++) {
+        if (w < warp) wb += s_wsum[w];
+        total += s_wsum[w];
+    }
+    const uint32_t excl = wb + x - sum;
+    if (threadIdx.x == 0) {
+        unsigned long long prefix = 0;
+        if (tile == 0) {
+            atomicExch(status, st_pack(epoch, 2, total));
+        } else {
+            atomicExch(status + tile, st_pack(epoch, 1, total));
+            int j = (int)tile - 1;
+            for (;;) {
+                const unsigned long long wv = atomicAdd(status + j, 0ull);
+                const uint32_t ep = (uint32_t)(wv >> 40), fl = (uint32_t)(wv >> 38) & 3u;
+                if (ep != (epoch & 0xFFFFFFu) || fl == 0) {
+                    __nanosleep(32);
+                    continue;
+                }
+                prefix += wv & ((1ull << 38) - 1);
+                if (fl == 2) break;
+                j--;
+            }
+            atomicExch(status + tile, st_pack(epoch, 2, prefix + total));
+        }
+        s_prefix = prefix;
+        if (tile == nt - 1) {
+            const unsigned long long K = prefix + total;
+            ctr[C_NKEYS] = K;
+            ctr[C_KCLAMP] = K < cap ? K : cap;
+            if (K > cap) ctr[C_OVF] = K;
+            atomicMax(ctr + C_MAXK, K);
+            ctr[C_EMITK] += K;
+        }
+    }
+    __syncthreads();
+    unsigned long long o = s_prefix + excl;
+#pragma unroll
+    for (int k = 0; k < kEmitPer; k++) {
+        if (base + k >= m || cnt[k] == 0) continue;
+        const uint32_t r = a + base + k;
         const SplatRec s = rec_sorted[r];
         const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
         const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
-        uint64_t o = off[i];
         for (uint32_t ty = y0; ty <= y1; ty++)
             for (uint32_t tx = x0; tx <= x1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
@@ -187,6 +302,7 @@ void work_free(RenderWork* w) {
     free_ptr(w->range);
     free_ptr(w->state);
     free_ptr(w->tile_done);
+    free_ptr(w->status);
     free_ptr(w->hist);
     free_ptr(w->ctr);
     if (w->h_ctr) cudaFreeHost(w->h_ctr);
@@ -197,6 +313,8 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
     if (!w->ctr) {
         GSV_CUDA(cudaMalloc(&w->ctr, 16 * sizeof(unsigned long long)));
         GSV_CUDA(cudaMallocHost(&w->h_ctr, 16 * sizeof(unsigned long long)));
+        GSV_CUDA(cudaMemset(w->ctr, 0, 16 * sizeof(unsigned long long)));
+        memset(w->h_ctr, 0, 16 * sizeof(unsigned long long));
     }
     n = std::max<int64_t>(n, 1);
     if (n > w->cap_n) {
@@ -213,6 +331,11 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
         GSV_CUDA(cudaMalloc(&w->rec_sorted, c * sizeof(SplatRec)));
         GSV_CUDA(cudaMalloc(&w->cnt, (c + 1) * sizeof(uint32_t)));
+        free_ptr(w->status);
+        const size_t ns = (size_t)(c / 256 + 4) * sizeof(unsigned long long) + 64;
+        GSV_CUDA(cudaMalloc(&w->status, ns));
+        GSV_CUDA(cudaMemset(w->status, 0, ns));
+        w->ticket = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(w->status) + ns - 64);
         w->cap_n = c;
     }
     k = std::max<int64_t>(k, 1 << 16);
@@ -288,9 +411,10 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
-        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], ctr);
-        radix_sort<uint64_t>(w->dkey, w->didx, ctr + C_N, w->cap_n, 8, npass, w->hist, digit_total, s);
-        count_launch(1 + 3 * 8);
+        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr);
+        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, w->hist, digit_total, s);
+        depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
+        count_launch(2 + 3 * 4);
     }
     prof_mark(ST_EMIT, s);
     const unsigned g = 148 * 4;
@@ -303,20 +427,17 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     for (size_t j = 0; j + 1 < bounds.size(); j++) {
         const uint32_t a = bounds[j], b = bounds[j + 1];
         prof_mark(ST_EMIT, s);
-        round_count<<<g, 256, 0, s>>>(w->rec_sorted, ctr, a, b, w->tile_done, w->cnt, ntx);
-        exclusive_scan(w->cnt, ctr + C_RN, (int64_t)(b - a), w->hist, ctr + C_NKEYS, s);
-        round_emit<<<g, 256, 0, s>>>(w->rec_sorted, w->cnt, ctr, a, w->tile_done, w->tkey[0], w->tval[0],
-                                     (uint64_t)w->cap_k, ntx);
-        count_launch(5);
+        const unsigned ge = (unsigned)((b - a + kEmitTile - 1) / kEmitTile);
+        round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b, w->tile_done, w->tkey[0],
+                                                      w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
+                                                      w->ticket, ++w->epoch);
+        count_launch(1);
         prof_mark(ST_TSORT, s);
         radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, w->hist, digit_total, s);
         count_launch(3 * tp);
-        prof_mark(ST_RANGES, s);
-        cudaMemsetAsync(w->range, 0, (size_t)ntiles * 2 * sizeof(uint32_t), s);
-        tile_ranges<<<g, 256, 0, s>>>(w->tkey[tp & 1], ctr, w->range);
-        count_launch(1);
         prof_mark(ST_COMPOSITE, s);
-        launch_composite_round(w->tval[tp & 1], w->range, w->rec_sorted, w->state, w->tile_done, cam, s);
+        launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+                               w->tile_done, cam, s);
         count_launch(1);
     }
     launch_finalize(w->state, cam, out_rgb, out_rgb8, s);
@@ -387,7 +508,7 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s) {
     const int64_t n = src.n;
-    int rc = work_reserve(w, n, w->cap_k, 1, 0);
+    int rc = work_reserve(w, n, std::max<int64_t>(w->cap_k, n), 1, 0);
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
@@ -395,8 +516,9 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
     reset_ctr_kernel<<<1, 1, 0, s>>>(ctr, (long long)n);
     launch_project_soa(src, cam, w, rects, depth, s);
     if (n > 0) {
-        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], ctr);
-        radix_sort<uint64_t>(w->dkey, w->didx, ctr + C_N, w->cap_n, 8, npass, w->hist, digit_total, s);
+        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr);
+        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, w->hist, digit_total, s);
+        depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         copy_order<<<148 * 4, 256, 0, s>>>(w->didx[0], w->didx[1], ctr, order, w->rec, tile_count);
     }
     cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);

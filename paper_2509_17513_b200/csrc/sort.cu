@@ -18,7 +18,7 @@ namespace gsv {
 
 constexpr int kRadix = 256;
 constexpr int kThreads = 256;
-constexpr int kRounds = 8;
+constexpr int kRounds = 2;
 constexpr int kTileItems = kThreads * kRounds;  // 2048
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
