@@ -285,8 +285,8 @@ struct gsv_video {
     int nslots = 0;
     DevBuf d_payload;             // staged bytes (empty when resident)
     RunSet runs;
-    DevBuf d_slots;               // [group][layer][slot]
-    std::vector<size_t> group_slot_base;
+    DevBuf d_slots;               // [frame (group-major)][layer][slot]
+    std::vector<size_t> frame_base;  // by group-major frame number
     std::vector<std::vector<uint32_t>> layer_off;  // per group prefix sums
     int64_t frame_total = 0;
 };
@@ -436,30 +436,34 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     }
     if (best.set()) return bail(fail(best.kind, best.msg));
 
-    // ---- frame tables ---------------------------------------------------------
+    // ---- frame tables: per frame, per layer, per slot the resolved plane ----
     std::vector<SlotDesc> sd;
-    v->group_slot_base.resize(G);
+    v->frame_base.clear();
     v->layer_off.resize(G);
     for (int g = 0; g < G; g++) {
-        v->group_slot_base[g] = sd.size();
         auto& lo2 = v->layer_off[g];
         lo2.assign(k + 1, 0);
-        for (int l = 0; l < k; l++) {
-            lo2[l + 1] = lo2[l] + c.groups[g].layer_counts[l];
-            for (int sl = 0; sl < v->nslots; sl++) {
-                SlotDesc d{};
-                const SlotRef& ref = slots[g][l][sl];
-                if (ref.run >= 0) {
-                    d.rmin = (double)ref.e->rmin;
-                    d.rmax = (double)ref.e->rmax;
-                    d.plane_base = v->runs.runs[ref.run].plane_base;
-                    d.dir_bits = ref.e->bits;
-                    d.bits = v->runs.runs[ref.run].bits;
-                }
-                sd.push_back(d);
-            }
-        }
+        for (int l = 0; l < k; l++) lo2[l + 1] = lo2[l] + c.groups[g].layer_counts[l];
         v->frame_total += c.groups[g].frame_count;
+    }
+    for (int g = 0; g < G; g++) {
+        for (int f = 0; f < c.groups[g].frame_count; f++) {
+            v->frame_base.push_back(sd.size());
+            for (int l = 0; l < k; l++)
+                for (int sl = 0; sl < v->nslots; sl++) {
+                    SlotDesc d{};
+                    const SlotRef& ref = slots[g][l][sl];
+                    if (ref.run >= 0) {
+                        const RunDesc& rd = v->runs.runs[ref.run];
+                        d.samples = v->runs.planes[rd.plane_base + f].samples;
+                        d.rmin = (double)ref.e->rmin;
+                        d.span = (double)ref.e->rmax - (double)ref.e->rmin;
+                        d.dir_bits = ref.e->bits;
+                        d.bits = rd.bits;
+                    }
+                    sd.push_back(d);
+                }
+        }
     }
     if ((rc = upload(v->d_slots, sd, st))) return bail(rc);
     GSV_CUDA(cudaStreamSynchronize(st));
@@ -473,9 +477,9 @@ int frame_src(gsv_video* v, int t, FrameSrc* src) {
         const GroupDir& gd = c.groups[g];
         if ((int64_t)gd.start_frame <= t && t < (int64_t)gd.start_frame + gd.frame_count) {
             memset(src, 0, sizeof *src);
-            src->slots = v->d_slots.as<SlotDesc>() + v->group_slot_base[g];
-            src->planes = v->runs.d_planes.as<PlaneRef>();
-            src->frame = t - (int)gd.start_frame;
+            size_t fi = 0;  // group-major frame number of (g, t - start)
+            for (size_t h = 0; h < g; h++) fi += c.groups[h].frame_count;
+            src->slots = v->d_slots.as<SlotDesc>() + v->frame_base[fi + (t - gd.start_frame)];
             src->nlayers = v->k;
             src->nslots = v->nslots;
             src->sh_degree = c.sh_degree;

@@ -30,12 +30,17 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__
     return lo;
 }
 
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 __global__ void __launch_bounds__(256) composite_round_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx) {
-    __shared__ float4 s_a[256], s_b[256];
-    __shared__ uint4 s_c[256];
+    __shared__ __align__(16) float4 s_rec[256 * 4];  // 256 staged 64-B records
     __shared__ uint32_t s_range[2];
     const int tile = blockIdx.x;
     if (threadIdx.x < 2) {  // this tile's [start, end) in the tile-sorted keys
@@ -45,11 +50,14 @@ __global__ void __launch_bounds__(256) composite_round_kernel(
     __syncthreads();
     const uint32_t start = s_range[0], end = s_range[1];
     if (start >= end) return;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_rec);
     const int tx = tile % ntx, ty = tile / ntx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // warp w owns an 8x4 pixel block of the 16x16 tile
     const int bx0 = tx * kTile + (warp & 1) * 8, by0 = ty * kTile + (warp >> 1) * 4;
     const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+    const float pxf = (float)px, pyf = (float)py;
+    const float bx0f = (float)bx0, by0f = (float)by0;
     const bool inside = px < width && py < height;
     const size_t pix = (size_t)py * width + px;
     float4 st = inside ? state[pix] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -60,9 +68,8 @@ __global__ void __launch_bounds__(256) composite_round_kernel(
         const uint32_t j = base + threadIdx.x;
         if (j < end) {
             const float4* r = reinterpret_cast<const float4*>(recs + ranks[j]);
-            s_a[threadIdx.x] = __ldg(r);
-            s_b[threadIdx.x] = __ldg(r + 1);
-            s_c[threadIdx.x] = __ldg(reinterpret_cast<const uint4*>(r + 2));
+#pragma unroll
+            for (int k = 0; k < 4; k++) s_rec[threadIdx.x * 4 + k] = __ldg(r + k);
         }
         __syncthreads();
         const int cnt = (int)min(256u, end - base);
@@ -71,33 +78,31 @@ __global__ void __launch_bounds__(256) composite_round_kernel(
             // which of the next 32 records touch this warp's 8x4 block?
             bool hit = false;
             if (g + lane < cnt) {
-                const uint4 c = s_c[g + lane];
-                const int x0 = (int)(c.y & 0xFFFFu), x1 = (int)(c.y >> 16);
-                const int y0 = (int)(c.z & 0xFFFFu), y1 = (int)(c.z >> 16);
-                hit = x0 < bx0 + 8 && x1 > bx0 && y0 < by0 + 4 && y1 > by0;
+                const float4 rc = lds_f4(sbase + (uint32_t)(g + lane) * 64u);
+                hit = rc.x < bx0f + 8.0f && rc.z > bx0f && rc.y < by0f + 4.0f && rc.w > by0f;
             }
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
             while (mask) {
-                const int q = g + __ffs(mask) - 1;
+                const uint32_t q = (uint32_t)(g + __ffs(mask) - 1);
                 mask &= mask - 1;
                 if (done) continue;
-                const uint4 c = s_c[q];  // op bits, rx, ry, pad
-                const int ix = px - (int)(c.y & 0xFFFFu), iy = py - (int)(c.z & 0xFFFFu);
-                if ((unsigned)ix >= (c.y >> 16) - (c.y & 0xFFFFu) ||
-                    (unsigned)iy >= (c.z >> 16) - (c.z & 0xFFFFu))
-                    continue;  // outside the splat's integer rect (render.py:313-315)
+                const uint32_t ra = sbase + q * 64u;
+                const float4 rc = lds_f4(ra);  // x0, y0, x1, y1
+                // outside the splat's integer rect (render.py:313-315)
+                if (pxf < rc.x || pxf >= rc.z || pyf < rc.y || pyf >= rc.w) continue;
                 if (T < 1e-4f) {
                     done = true;
                     continue;
                 }
-                const float4 a = s_a[q];  // ox, oy, ca, cb
-                const float4 b = s_b[q];  // cc, r, g, b
-                const float dx = (float)ix - a.x;
-                const float dy = (float)iy - a.y;
+                const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
+                const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
+                const float op = lds_f4(ra + 48u).x;
+                const float dx = (pxf - rc.x) - a.x;
+                const float dy = (pyf - rc.y) - a.y;
                 const float pw = fminf(fmaf(fmaf(a.z, dx, a.w * dy), dx, b.x * dy * dy), 0.0f);
                 float e;
                 asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw));
-                const float alpha = fminf(__uint_as_float(c.x) * e, 0.99f);
+                const float alpha = fminf(op * e, 0.99f);
                 if (alpha <= 0.0f) continue;
                 const float w = T * alpha;
                 c0 = fmaf(w, b.y, c0);

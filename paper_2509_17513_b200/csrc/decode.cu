@@ -144,7 +144,7 @@ __device__ __forceinline__ uint32_t load_sample(const uint8_t* p, uint32_t j, in
 
 __device__ __forceinline__ double dequant(uint32_t code, const SlotDesc& sd) {
     const double top = sd.dir_bits >= 32 ? 4294967295.0 : (double)((1ull << sd.dir_bits) - 1ull);
-    return __dadd_rn(sd.rmin, __dmul_rn(__ddiv_rn((double)code, top), __dsub_rn(sd.rmax, sd.rmin)));
+    return __dadd_rn(sd.rmin, __dmul_rn(__ddiv_rn((double)code, top), sd.span));
 }
 
 __global__ void dequant_frame_kernel(FrameSrc src, double* __restrict__ pos, double* __restrict__ rot,
@@ -159,8 +159,7 @@ __global__ void dequant_frame_kernel(FrameSrc src, double* __restrict__ pos, dou
     const SlotDesc* sd = src.slots + (size_t)l * src.nslots;
     for (int s = 0; s < src.nslots; s++) {
         const SlotDesc d = sd[s];
-        const PlaneRef& pr = src.planes[d.plane_base + src.frame];
-        const double v = dequant(load_sample(pr.samples, j, d.bits), d);
+        const double v = dequant(load_sample(d.samples, j, d.bits), d);
         if (s < 3) pos[3 * (size_t)i + s] = v;
         else if (s < 7) rot[4 * (size_t)i + (s - 3)] = v;
         else if (s < 10) scl[3 * (size_t)i + (s - 7)] = v;
@@ -186,8 +185,7 @@ __global__ void frame_codes_kernel(FrameSrc src, uint32_t* __restrict__ out) {
     const uint32_t i = src.layer_off[l] + j;
     const SlotDesc* sd = src.slots + (size_t)l * src.nslots;
     for (int s = 0; s < src.nslots; s++) {
-        const PlaneRef& pr = src.planes[sd[s].plane_base + src.frame];
-        out[(size_t)i * src.nslots + s] = load_sample(pr.samples, j, sd[s].bits);
+        out[(size_t)i * src.nslots + s] = load_sample(sd[s].samples, j, sd[s].bits);
     }
 }
 

@@ -93,20 +93,20 @@ struct PlaneRef {
     uint32_t mode;           // 0: range coded, 1: raw
 };
 
-// Per (group, layer, slot) dequantization parameters + the run providing it.
+// One (frame, layer, slot): where that frame's codes live and how to
+// dequantize them (quantize.py:114-117 with span = rmax - rmin).
 struct SlotDesc {
-    double rmin, rmax;      // directory range (f32 values promoted)
-    uint32_t plane_base;    // PlaneRef index of frame 0 of the run
-    uint8_t dir_bits;       // directory bit width -> top = 2^bits - 1
-    uint8_t bits;           // payload sample width
-    uint16_t pad;
+    const uint8_t* samples;  // little-endian plane samples of this frame (device)
+    double rmin, span;       // directory range (f32 values promoted), rmax - rmin
+    uint8_t dir_bits;        // directory bit width -> top = 2^bits - 1
+    uint8_t bits;            // payload sample width
+    uint16_t pad0;
+    uint32_t pad1;
 };
 
-// A frame's source: `nlayers` layers of its group.
+// A frame's source: its resolved slots [nlayers][nslots].
 struct FrameSrc {
-    const SlotDesc* slots;       // [nlayers][nslots] for the frame's group
-    const PlaneRef* planes;      // all PlaneRefs
-    int32_t frame;               // frame index inside its group
+    const SlotDesc* slots;
     int32_t nlayers;
     int32_t nslots;
     int32_t sh_degree;
@@ -134,13 +134,15 @@ struct CamDev {
     int32_t width, height;
 };
 
-// 48-byte splat record consumed by the compositor (all fp32):
-//   ox, oy : mean - rect origin (px)
-//   ca, cb, cc : -log2(e)/2 * (a, 2b, c) of the conic inverse (render.py:346-349),
-//                so alpha = op * 2^(ca dx^2 + cb dx dy + cc dy^2)
-//   r, g, b: SH colour in [0,1]             op : opacity
-//   rx, ry : x0 | x1 << 16, y0 | y1 << 16   (u16 each)
+// 64-byte splat record consumed by the compositor:
+//   fx0, fy0, fx1, fy1 : the integer rect [x0, x1) x [y0, y1) as floats (exact)
+//   ox, oy             : mean - rect origin (px)
+//   ca, cb, cc         : -log2(e)/2 * (a, 2b, c) of the conic inverse
+//                        (render.py:346-349): alpha = op * 2^(ca dx^2 + cb dx dy + cc dy^2)
+//   r, g, b            : SH colour in [0, 1];  op : opacity
+//   rx, ry             : x0 | x1 << 16, y0 | y1 << 16 (u16 each; tile binning)
 struct __align__(16) SplatRec {
+    float fx0, fy0, fx1, fy1;
     float ox, oy, ca, cb;
     float cc, r, g, b;
     float op;

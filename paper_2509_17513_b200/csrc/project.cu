@@ -44,7 +44,7 @@ __device__ __forceinline__ double dequant_p(uint32_t code, const SlotDesc& sd) {
     else if (sd.dir_bits == 16 && code < 65536u) q = __ldg(g_q16 + code);
     else q = __ddiv_rn((double)code, sd.dir_bits >= 32 ? 4294967295.0
                                                         : (double)((1ull << sd.dir_bits) - 1ull));
-    return __dadd_rn(sd.rmin, __dmul_rn(q, __dsub_rn(sd.rmax, sd.rmin)));
+    return __dadd_rn(sd.rmin, __dmul_rn(q, sd.span));
 }
 
 static void init_quotient_tables() {
@@ -80,7 +80,7 @@ struct PlaneLoader {
 #pragma unroll
         for (int s = S0; s < S1; s++) {
             const SlotDesc d = sd[s];
-            const double v = dequant_p(load_sample_p(src.planes[d.plane_base + src.frame].samples, j, d.bits), d);
+            const double v = dequant_p(load_sample_p(d.samples, j, d.bits), d);
             if (s < 3) a.p[s] = v;
             else if (s < 7) a.q[s - 3] = v;
             else if (s < 10) a.s[s - 7] = v;
@@ -275,6 +275,10 @@ __global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
             sh_color(a, cam, rgb);
             const double det = o.cov[0] * o.cov[3] - o.cov[1] * o.cov[1];
             SplatRec r;
+            r.fx0 = (float)o.x0;
+            r.fy0 = (float)o.y0;
+            r.fx1 = (float)o.x1;
+            r.fy1 = (float)o.y1;
             r.ox = (float)(o.u - o.x0);
             r.oy = (float)(o.v - o.y0);
             // conic (render.py:346-349) folded into the base-2 exponent the

@@ -377,18 +377,17 @@ static int tile_passes(int ntiles) {
     return std::max(1, (bits + 7) / 8);
 }
 
-// Depth-rank rounds: [0, 32k), [32k, 128k), [128k, 512k), ... Tiles saturate
-// within the first few tens of thousands of ranks (~97
-// evaluations per covered pixel), so later rounds only emit keys for the
-// few tiles that are still open.
+// Depth-rank rounds: [0, R1) for every tile, then [R1, n) only for the tiles
+// still open.  Tiles saturate within the first ~10-30k ranks at config 2
+// (~97 evaluations per covered pixel), so the second round
+// emits keys only for the few tiles that never saturate: 1.08M keys instead
+// of 7.18M at config 2 (measured with the oracle, tools/analysis notes in
+// DESIGN.md).
 static void round_bounds(int64_t n, std::vector<uint32_t>* b) {
     b->clear();
-    uint64_t x = 0, step = 32768;
-    while ((int64_t)x < n) {
-        b->push_back((uint32_t)x);
-        x += step;
-        step *= 4;
-    }
+    const int64_t r1 = std::max<int64_t>(32768, n / 10);
+    b->push_back(0);
+    if (n > r1) b->push_back((uint32_t)r1);
     b->push_back((uint32_t)std::max<int64_t>(n, 0));
 }
 
