@@ -235,12 +235,8 @@ struct RunSet {
             const int nb = runs[i].bits / 8;
             rc_runs[nb == 1 ? 0 : (nb == 2 ? 1 : 2)].push_back((uint32_t)i);
         }
-        std::vector<uint32_t> rc_all, rc_start(4, 0);
-        for (int b = 0; b < 3; b++) {
-            rc_start[b] = (uint32_t)rc_all.size();
-            rc_all.insert(rc_all.end(), rc_runs[b].begin(), rc_runs[b].end());
-        }
-        rc_start[3] = (uint32_t)rc_all.size();
+        std::vector<uint32_t> rc_all;
+        for (int b = 0; b < 3; b++) rc_all.insert(rc_all.end(), rc_runs[b].begin(), rc_runs[b].end());
         std::vector<uint32_t> chunk_prefix(planes.size() + 1, 0);
         for (size_t i = 0; i < planes.size(); i++) {
             const uint32_t pb = runs[planes[i].run].plane_bytes;
@@ -252,16 +248,12 @@ struct RunSet {
         if ((rc = upload(d_chunk, chunk_prefix, s))) return rc;
         if ((rc = d_crc.alloc(std::max<size_t>(runs.size(), 1) * 4))) return rc;
         GSV_CUDA(cudaMemsetAsync(d_crc.p, 0, std::max<size_t>(runs.size(), 1) * 4, s));
-        const int nbytes_of[3] = {1, 2, 4};
         prof_mark(ST_RCDEC, s);
         launch_copy_planes(d_jobs.as<CopyJob>(), (int)jobs.size(), s);
         if (!jobs.empty()) count_launch();
-        for (int b = 0; b < 3; b++) {
-            const int n = (int)(rc_start[b + 1] - rc_start[b]);
-            launch_rc_decode(d_runs.as<RunDesc>(), d_rc.as<uint32_t>() + rc_start[b], n,
-                             d_planes.as<PlaneRef>(), nbytes_of[b], s);
-            if (n > 0) count_launch();
-        }
+        const int n_cls[3] = {(int)rc_runs[0].size(), (int)rc_runs[1].size(), (int)rc_runs[2].size()};
+        launch_rc_decode(d_runs.as<RunDesc>(), d_rc.as<uint32_t>(), n_cls, d_planes.as<PlaneRef>(), s);
+        if (!rc_all.empty()) count_launch();
         prof_mark(ST_CRC, s);
         launch_crc(d_runs.as<RunDesc>(), d_planes.as<PlaneRef>(), (int)planes.size(),
                    d_chunk.as<uint32_t>(), chunk_prefix.back(), d_crc.as<uint32_t>(), s);

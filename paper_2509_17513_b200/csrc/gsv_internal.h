@@ -196,8 +196,9 @@ struct CopyJob {
 // rc_decode.cu
 void launch_copy_planes(const CopyJob* jobs, int njobs, cudaStream_t s);
 // decode.cu
-void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, int n_rc_runs,
-                      const PlaneRef* planes, int nbytes, cudaStream_t s);
+// rc_runs: run indices grouped by sample width (1, 2, 4 bytes), n_per_class[3]
+void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
+                      const PlaneRef* planes, cudaStream_t s);
 void launch_crc(const RunDesc* runs, const PlaneRef* planes, int nplanes,
                 const uint32_t* plane_chunk_prefix, uint32_t nchunks, uint32_t* run_crc,
                 cudaStream_t s);

@@ -97,17 +97,18 @@ struct CodedStream {
     }
 };
 
-// Probabilities: node i of a tree lives in quad (i >> 2), element (i & 3) of
-// the lane's column (u32, layout [tree][quad][lane][4]).  At node c the quad
-// c holds its four grandchildren, so one 128-bit shared load issued at the
-// start of decision k delivers every probability decision k+1 can need: the
-// load has two decisions to land and never sits on the bit-serial chain.
-// The quad holding the *children* of c was loaded one decision earlier.
+// Probabilities: lane-private, tree after tree, node n of a tree at byte
+// offset 4n (so node addresses are one LEA and the quad of grandchildren
+// 4c..4c+3 of node c is one aligned 128-bit load at offset 16c); lanes are
+// kLaneStride apart, skewed by 16 B so that the lanes' quad loads spread over
+// the banks.  At node c the quad c holds its four grandchildren: one load
+// issued at decision k delivers every probability decision k+1 can need, so
+// the load has two decisions to land and never sits on the bit-serial chain.
 // Shared accesses are volatile PTX so the compiler neither converts the
 // speculative loads into bit-dependent ones nor reorders them around the
-// probability updates.
-constexpr uint32_t kQuadStride = 16u * kRPW;        // bytes between quads of one lane
-constexpr uint32_t kTreeStride = 64u * kQuadStride;  // 64 quads per tree
+// probability stores.
+constexpr uint32_t kTreeBytes = 256u * 4u;
+__host__ __device__ constexpr uint32_t lane_stride(int nb) { return (uint32_t)nb * kTreeBytes + 16u; }
 
 __device__ __forceinline__ uint4 lds_quad(uint32_t addr) {
     uint4 v;
@@ -119,30 +120,35 @@ __device__ __forceinline__ uint4 lds_quad(uint32_t addr) {
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
-__device__ __forceinline__ uint32_t node_addr(uint32_t tree, uint32_t node) {
-    return tree + (node >> 2) * kQuadStride + (node & 3) * 4u;
+__device__ __forceinline__ uint32_t node_addr(uint32_t tree, uint32_t node) { return tree + node * 4u; }
+
+// Adaptive update of one node (_rc.py:140-146): bit 0: p += (4096 - p) >> 4,
+// bit 1: p -= p >> 4.  Both are p + ((K - p) >> 4) with an arithmetic shift,
+// K = 4096 or 15 (floor((15 - p) / 16) == -floor(p / 16) for integer p).
+__device__ __forceinline__ uint32_t adapt(uint32_t p, bool bit) {
+    return p + (uint32_t)(((int32_t)(bit ? 15u : 4096u) - (int32_t)p) >> 4);
 }
 
-// 8 decisions of one byte on tree T.  q0 holds quad 0 of T on entry (nodes
-// 0..3: root + its children) and quad 0 of tree Tn on exit.
-__device__ __forceinline__ uint32_t decode_byte(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
-                                                uint32_t& code, CodedStream& cs) {
+// 8 decisions of one byte on tree T, careful path: every decision stores its
+// node and keeps >= 32 buffered bits (at most 32 are consumed per two
+// decisions).  q0 holds quad 0 of T on entry (node 1 and its children) and
+// quad 0 of tree Tn on exit.
+__device__ __forceinline__ uint32_t decode_byte_slow(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
+                                                     uint32_t& code, CodedStream& cs) {
     uint32_t ctx = 1;
     uint32_t p = q0.y;  // node 1
     uint4 cq = q0;      // quad holding the children of ctx
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         uint4 nq = make_uint4(0u, 0u, 0u, 0u);
-        if (k < 6) nq = lds_quad(T + ctx * kQuadStride);  // grandchildren of ctx
-        if (k == 6) q0 = lds_quad(Tn);                    // next byte's root quad
-        // children of ctx are elements 2*(ctx&1), +1 of cq
+        if (k < 6) nq = lds_quad(T + ctx * 16u);  // grandchildren of ctx
         const uint32_t c0 = (ctx & 1) ? cq.z : cq.x;
         const uint32_t c1 = (ctx & 1) ? cq.w : cq.y;
         const uint32_t bound = (rng >> 12) * p;
         const bool bit = code >= bound;
         code = bit ? code - bound : code;
         rng = bit ? rng - bound : bound;
-        sts_u32(node_addr(T, ctx), bit ? p - (p >> 4) : p + ((4096u - p) >> 4));
+        sts_u32(node_addr(T, ctx), adapt(p, bit));
         ctx = 2 * ctx + (bit ? 1u : 0u);
         p = bit ? c1 : c0;
         cq = nq;
@@ -152,8 +158,68 @@ __device__ __forceinline__ uint32_t decode_byte(uint32_t T, uint32_t Tn, uint4& 
         rng <<= sh;
         cs.bb <<= sh;
         cs.nbits -= (int32_t)sh;
-        if (k & 1) cs.refill();  // <= 32 bits consumed per two decisions
+        if (k & 1) cs.refill();
     }
+    q0 = lds_quad(Tn);  // after this byte's stores (Tn may be T)
+    return ctx & 0xFFu;
+}
+
+// Fast path: the byte's decisions read the coded bits at a running offset
+// into the 64-bit buffer (one funnel shift) and defer the 8 probability
+// stores to the end of the byte, so a decision is: multiply, compare, select,
+// renormalise -- no buffer bookkeeping, no store, no branch.  It is exact as
+// long as the byte consumes at most 32 bits (>= 33 are buffered at the start);
+// otherwise nothing has been written and the byte is redone on the careful
+// path from the saved state.  Multi-byte samples alternate trees, so q0 of
+// the next tree is loaded during this byte; for one-byte samples the next
+// root quad is this tree's, patched in registers with the new node 1..3.
+template <bool SAME_TREE>
+__device__ __forceinline__ uint32_t decode_byte(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
+                                                uint32_t& code, CodedStream& cs) {
+    const uint32_t rng0 = rng, code0 = code;
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32), blo = (uint32_t)cs.bb;
+    uint32_t ctx = 1, off = 0;
+    uint32_t p = q0.y;
+    uint4 cq = q0;
+    uint4 qn = q0;
+    uint32_t pn[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+        if (k < 6) nq = lds_quad(T + ctx * 16u);
+        if (!SAME_TREE && k == 6) qn = lds_quad(Tn);
+        const uint32_t c0 = (ctx & 1) ? cq.z : cq.x;
+        const uint32_t c1 = (ctx & 1) ? cq.w : cq.y;
+        const uint32_t bound = (rng >> 12) * p;
+        const bool bit = code >= bound;
+        code = bit ? code - bound : code;
+        rng = bit ? rng - bound : bound;
+        pn[k] = adapt(p, bit);
+        ctx = 2 * ctx + (bit ? 1u : 0u);
+        p = bit ? c1 : c0;
+        cq = nq;
+        const uint32_t sh = rng < (1u << 24) ? (rng < (1u << 16) ? 16u : 8u) : 0u;
+        code = __funnelshift_l(__funnelshift_lc(blo, bhi, off), code, sh);
+        rng <<= sh;
+        off += sh;
+    }
+    if (off > 32u) {  // rare: redo carefully (nothing was stored)
+        rng = rng0;
+        code = code0;
+        return decode_byte_slow(T, Tn, q0, rng, code, cs);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) sts_u32(node_addr(T, ctx >> (8 - k)), pn[k]);
+    if (SAME_TREE) {
+        const bool b0 = (ctx >> 7) & 1u;  // first decision: node 2 or 3 was updated second
+        qn.y = pn[0];
+        qn.z = b0 ? q0.z : pn[1];
+        qn.w = b0 ? pn[1] : q0.w;
+    }
+    q0 = qn;
+    cs.bb <<= off;
+    cs.nbits -= (int32_t)off;
+    cs.refill();
     return ctx & 0xFFu;
 }
 
@@ -205,8 +271,8 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
             uint32_t z = 0;
 #pragma unroll
             for (int b = 0; b < NB; b++)
-                z |= decode_byte(P + b * kTreeStride, P + ((b + 1) % NB) * kTreeStride, q0, rng, code,
-                                 cs) << (8 * b);
+                z |= decode_byte<NB == 1>(P + b * kTreeBytes, P + ((b + 1) % NB) * kTreeBytes, q0, rng,
+                                          code, cs) << (8 * b);
             const uint32_t v = (pred + ((z >> 1) ^ (0u - (z & 1u)))) & mask;  // unzigzag
             if (!PREV) {
                 if (x == 0) above = v;
@@ -220,17 +286,18 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
     }
 }
 
+// One launch for every width class (no serialisation of the u8 and u16 runs
+// behind each other): blocks [0, nb1) decode the 8-bit runs, the next nb2
+// blocks the 16-bit runs, the rest the 32-bit runs.  One warp per CTA, so
+// the warps land on separate SMs.
 template <int NB>
-__global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restrict__ runs,
-                                                         const uint32_t* __restrict__ rc_runs, int n,
-                                                         const PlaneRef* __restrict__ planes) {
-    extern __shared__ uint4 probs_s[];
+__device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, const uint32_t* __restrict__ rc_runs,
+                                            int n, int blk, const PlaneRef* __restrict__ planes, uint32_t P) {
     const int lane = threadIdx.x;
-    const uint32_t P = (uint32_t)__cvta_generic_to_shared(probs_s + lane);
     for (int b = 0; b < NB; b++)  // new_bittree_probs (_rc.py:304-317)
         for (uint32_t i = 0; i < 256; i++)
-            sts_u32(node_addr(P + b * kTreeStride, i), (i != 0 && (i & (i - 1)) == 0) ? 3686u : 2048u);
-    const int gi = blockIdx.x * kRPW + lane;
+            sts_u32(node_addr(P + b * kTreeBytes, i), (i != 0 && (i & (i - 1)) == 0) ? 3686u : 2048u);
+    const int gi = blk * kRPW + lane;
     if (gi >= n) return;
     const RunDesc r = runs[rc_runs[gi]];
     const uint32_t hw = (uint32_t)r.w * r.h;
@@ -247,20 +314,40 @@ __global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restri
     }
 }
 
-void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, int n, const PlaneRef* planes,
-                      int nbytes, cudaStream_t s) {
-    if (n <= 0) return;
-    const int blocks = (n + kRPW - 1) / kRPW;
-    const size_t smem = (size_t)nbytes * 256 * kRPW * 4;
-    if (nbytes == 1) {
-        rc_decode_kernel<1><<<blocks, kRPW, smem, s>>>(runs, rc_runs, n, planes);
-    } else if (nbytes == 2) {
-        cudaFuncSetAttribute(rc_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<2><<<blocks, kRPW, smem, s>>>(runs, rc_runs, n, planes);
-    } else {
-        cudaFuncSetAttribute(rc_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<4><<<blocks, kRPW, smem, s>>>(runs, rc_runs, n, planes);
+struct RcClasses {
+    int n[3];    // runs per class (1, 2, 4 bytes per sample)
+    int off[3];  // first index into rc_runs
+    int blk[4];  // block prefix
+};
+
+__global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restrict__ runs,
+                                                         const uint32_t* __restrict__ rc_runs, RcClasses c,
+                                                         const PlaneRef* __restrict__ planes) {
+    extern __shared__ uint4 probs_s[];
+    const int b = blockIdx.x;
+    const int nb = b < c.blk[1] ? 1 : (b < c.blk[2] ? 2 : 4);
+    const uint32_t P = (uint32_t)__cvta_generic_to_shared(probs_s) + threadIdx.x * lane_stride(nb);
+    if (b < c.blk[1]) decode_runs<1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P);
+    else if (b < c.blk[2]) decode_runs<2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P);
+    else decode_runs<4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P);
+}
+
+void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
+                      const PlaneRef* planes, cudaStream_t s) {
+    RcClasses c;
+    int nbmax = 0, off = 0;
+    c.blk[0] = 0;
+    for (int k = 0; k < 3; k++) {
+        c.n[k] = n_per_class[k];
+        c.off[k] = off;
+        off += c.n[k];
+        c.blk[k + 1] = c.blk[k] + (c.n[k] + kRPW - 1) / kRPW;
+        if (c.n[k] > 0) nbmax = 1 << k;
     }
+    if (c.blk[3] == 0) return;
+    const size_t smem = (size_t)lane_stride(nbmax) * kRPW;
+    cudaFuncSetAttribute(rc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rc_decode_kernel<<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
 }
 
 }  // namespace gsv
