@@ -1,18 +1,16 @@
 // Front-to-back alpha compositing over 16x16 tiles (render.py:301-356),
 // resumable across depth-rank rounds.
 //
-// One CTA per tile, one thread per pixel, each warp an 8x4 pixel block.  A
-// round hands every tile the
-// records of its splats whose depth ranks fall in the round's range, in rank
-// order; the pixel's (C, T) state is loaded from and stored back to
-// `state`, so running the rounds in order is the same per-pixel loop as the
-// reference's (render.py:307-332): integer rect clip, T < 1e-4 skip, power
-// clamp, 0.99 alpha cap, alpha <= 0 skip, fp32 accumulation in a fixed
-// order (deterministic).  Records are staged through shared memory 256 at a
-// time; each warp ballots 32 records at a time against its block's bounds
-// and walks only the hits, leaves as soon as its 32 pixels are saturated,
-// and the CTA stops once every pixel has saturated, marking the tile done so
-// later rounds emit no keys for it.
+// A round hands every tile the records of its splats whose depth ranks fall
+// in the round's range, in rank order.  Running the rounds in order is the
+// reference's per-pixel loop (render.py:307-332): integer rect clip,
+// T < 1e-4 skip, power clamp, 0.99 alpha cap, alpha <= 0 skip, fp32
+// accumulation in a fixed order (deterministic).  The first round starts
+// from (C, T) = (0, 1) in registers; a tile whose pixels all saturate is
+// finished on the spot (background blend, clip, u8 rounding: render.py:
+// 333-338, 356, 165-169) and marked done so later rounds emit no keys for
+// it; the others carry their (C, T) to the next round through `state`, and
+// the last round finishes every tile still open.
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -53,14 +51,18 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
-    int ntiles) {
+    int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
+    uint8_t* __restrict__ out_rgb8) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile; a CTA of 4 warps holds 4/kStrips tiles
     __shared__ __align__(16) float4 s_rec[4][32 * 4];
     __shared__ int s_unsat[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw = blockIdx.x * 4 + warp;
     const int tile = gw / kStrips, strip = gw % kStrips;
-    const bool on = tile < ntiles;
+    // saturated tiles were written out in an earlier round; blank ones too,
+    // unless this round brings them keys
+    const uint8_t td = (tile < ntiles && !first) ? tile_done[tile] : kTileOpen;
+    bool on = tile < ntiles && td != kTileSaturated;
     uint32_t bound = 0;
     if (on && lane < 2) bound = lower_bound_u32(keys, (uint32_t)*nkeys, (uint32_t)tile + lane);
     const uint32_t start = __shfl_sync(0xffffffffu, bound, 0), end = __shfl_sync(0xffffffffu, bound, 1);
@@ -70,19 +72,26 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const int py0 = sy0 + (lane >> 4) * ROWS;        // this lane's first row
     const float pxf = (float)px, py0f = (float)py0;
     float T[ROWS], c0[ROWS], c1[ROWS], c2[ROWS];
-    uint32_t live = 0;
+    uint32_t live = 0, inimg = 0;
     const bool work = on && start < end;
+    if (td == kTileBlank && !work) on = false;  // still background, already written
+    // state I/O: the first round and blank tiles start from (0, 1); open tiles
+    // load it when they have keys or must be finished
+    const bool load = on && !first && td == kTileOpen && (work || last);
 #pragma unroll
     for (int j = 0; j < ROWS; j++) {
-        T[j] = 0.f;
+        T[j] = 1.f;
         c0[j] = c1[j] = c2[j] = 0.f;
-        if (work && px < width && py0 + j < height) {
-            const float4 st = state[(size_t)(py0 + j) * width + px];
-            c0[j] = st.x;
-            c1[j] = st.y;
-            c2[j] = st.z;
-            T[j] = st.w;
-            if (st.w >= 1e-4f) live |= 1u << j;
+        if (on && px < width && py0 + j < height) {
+            inimg |= 1u << j;
+            if (load) {
+                const float4 st = state[(size_t)(py0 + j) * width + px];
+                c0[j] = st.x;
+                c1[j] = st.y;
+                c2[j] = st.z;
+                T[j] = st.w;
+            }
+            if (T[j] >= 1e-4f) live |= 1u << j;
         }
     }
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(&s_rec[warp][0]);
@@ -133,60 +142,40 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
         }
         __syncwarp();
     }
-    bool sat = true;
-#pragma unroll
-    for (int j = 0; j < ROWS; j++) {
-        if (work && px < width && py0 + j < height) {
-            state[(size_t)(py0 + j) * width + px] = make_float4(c0[j], c1[j], c2[j], T[j]);
-            sat = sat && T[j] < 1e-4f;
-        }
-    }
-    // a tile is done once all its in-image pixels are saturated; tiles this
-    // round did not touch keep their flag (they were either done already or
-    // receive keys in a later round)
-    const bool wsat = __all_sync(0xffffffffu, sat);
-    if constexpr (kStrips == 1) {
-        if (work && wsat && lane == 0) tile_done[tile] = 1;
-    } else {
-        if (lane == 0) s_unsat[warp] = work ? (wsat ? 0 : 1) : 2;
+    const bool wsat = __all_sync(0xffffffffu, (live & inimg) == 0);
+    bool tsat = wsat;
+    if constexpr (kStrips > 1) {
+        if (lane == 0) s_unsat[warp] = wsat ? 0 : 1;
         __syncthreads();
-        if (on && strip == 0 && lane == 0) {
-            bool any_work = false, all_sat = true;
-            for (int k = 0; k < kStrips; k++) {
-                const int u = s_unsat[warp + k];
-                any_work |= u != 2;
-                all_sat &= u != 1;
-            }
-            if (any_work && all_sat) tile_done[tile] = 1;
-        }
+        const int w0 = warp - strip;
+        for (int k = 0; k < kStrips; k++) tsat = tsat && s_unsat[w0 + k] == 0;
     }
-}
-
-__global__ void state_init_kernel(float4* __restrict__ state, uint8_t* __restrict__ tile_done,
-                                  size_t npix, int ntiles) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < npix) state[i] = make_float4(0.f, 0.f, 0.f, 1.f);
-    if (i < (size_t)ntiles) tile_done[i] = 0;
-}
-
-// background blend + clip (render.py:333-338, 356) and optional u8 like write_ppm
-__global__ void finalize_kernel(const float4* __restrict__ state, size_t npix, float bg0, float bg1,
-                                float bg2, float* __restrict__ out_rgb, uint8_t* __restrict__ out_rgb8) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= npix) return;
-    const float4 s = state[i];
-    const float v[3] = {s.x + s.w * bg0, s.y + s.w * bg1, s.z + s.w * bg2};
+    if (!on) return;
+    // finish the tile (background blend, clip: render.py:333-338, 356) when
+    // it saturated, in the last round, and as blank background when the first
+    // round brought it no key; otherwise carry (C, T) to the next round
+    const bool blank = first && !work && !last;
+    if (last || tsat || blank) {
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-        const float x = fminf(fmaxf(v[k], 0.0f), 1.0f);
-        if (out_rgb) out_rgb[3 * i + k] = x;
-        if (out_rgb8) out_rgb8[3 * i + k] = (uint8_t)floorf(x * 255.0f + 0.5f);
+        for (int j = 0; j < ROWS; j++) {
+            if (!((inimg >> j) & 1u)) continue;
+            const size_t pix = (size_t)(py0 + j) * width + px;
+            const float v[3] = {fmaf(T[j], bg0, c0[j]), fmaf(T[j], bg1, c1[j]), fmaf(T[j], bg2, c2[j])};
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const float x = fminf(fmaxf(v[k], 0.0f), 1.0f);
+                if (out_rgb) out_rgb[3 * pix + k] = x;
+                if (out_rgb8) out_rgb8[3 * pix + k] = (uint8_t)floorf(x * 255.0f + 0.5f);
+            }
+        }
+        if (strip == 0 && lane == 0 && !last) tile_done[tile] = tsat ? kTileSaturated : kTileBlank;
+    } else if (work) {
+#pragma unroll
+        for (int j = 0; j < ROWS; j++)
+            if ((inimg >> j) & 1u)
+                state[(size_t)(py0 + j) * width + px] = make_float4(c0[j], c1[j], c2[j], T[j]);
+        if (strip == 0 && lane == 0 && td != kTileOpen) tile_done[tile] = kTileOpen;
     }
-}
-
-void launch_state_init(float4* state, uint8_t* tile_done, size_t npix, int ntiles, cudaStream_t s) {
-    const size_t n = npix > (size_t)ntiles ? npix : (size_t)ntiles;
-    state_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(state, tile_done, npix, ntiles);
 }
 
 static int composite_rows() {
@@ -201,28 +190,21 @@ static int composite_rows() {
 
 void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
                             const unsigned long long* nkeys, const SplatRec* recs, float4* state,
-                            uint8_t* tile_done, const CamDev& cam, cudaStream_t s) {
+                            uint8_t* tile_done, const CamDev& cam, bool first, bool last, float* out_rgb,
+                            uint8_t* out_rgb8, cudaStream_t s) {
     const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
     const int ntiles = ntx * nty;
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
     const unsigned grid = (unsigned)((warps + 3) / 4);
-    if (rows == 8)
-        composite_strip_kernel<8><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width,
-                                                        cam.height, ntx, ntiles);
-    else if (rows == 4)
-        composite_strip_kernel<4><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width,
-                                                        cam.height, ntx, ntiles);
-    else
-        composite_strip_kernel<2><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width,
-                                                        cam.height, ntx, ntiles);
-}
-
-void launch_finalize(const float4* state, const CamDev& cam, float* out_rgb, uint8_t* out_rgb8,
-                     cudaStream_t s) {
-    const size_t npix = (size_t)cam.width * cam.height;
-    finalize_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(state, npix, cam.bg[0], cam.bg[1],
-                                                                   cam.bg[2], out_rgb, out_rgb8);
+#define GSV_COMPOSITE(R)                                                                             \
+    composite_strip_kernel<R><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
+                                                   cam.height, ntx, ntiles, first, last, cam.bg[0],   \
+                                                   cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
+    if (rows == 8) GSV_COMPOSITE(8);
+    else if (rows == 4) GSV_COMPOSITE(4);
+    else GSV_COMPOSITE(2);
+#undef GSV_COMPOSITE
 }
 
 }  // namespace gsv

@@ -173,9 +173,11 @@ struct RenderWork {
     unsigned long long* status = nullptr;
     unsigned int* ticket = nullptr;
     uint32_t epoch = 0;
-    // radix / scan scratch
-    uint32_t* hist = nullptr;
-    int64_t hist_cap = 0;
+    // radix sort scratch (sort.cuh SortScratch)
+    uint32_t* sort_ghist = nullptr;              // 4 x 256 digit counts + ticket
+    unsigned long long* sort_status = nullptr;   // look-back status words
+    int64_t sort_status_cap = 0;
+    uint32_t sort_epoch = 0;
     // device counters: [0] n_visible, [1] n_keys, [2..3] depth min (u64), [4..5] depth max,
     // [6] key overflow flag, [8..] radix pass state
     unsigned long long* ctr = nullptr;
@@ -207,12 +209,13 @@ void launch_dequant_frame(const FrameSrc& src, double* pos, double* rot, double*
 void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
 
 // composite.cu
-void launch_state_init(float4* state, uint8_t* tile_done, size_t npix, int ntiles, cudaStream_t s);
+// One depth-rank round; `first` starts from (C, T) = (0, 1), `last` writes the
+// final image of every tile still open (saturated tiles are written when they
+// saturate).
 void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
                             const unsigned long long* nkeys, const SplatRec* recs, float4* state,
-                            uint8_t* tile_done, const CamDev& cam, cudaStream_t s);
-void launch_finalize(const float4* state, const CamDev& cam, float* out_rgb, uint8_t* out_rgb8,
-                     cudaStream_t s);
+                            uint8_t* tile_done, const CamDev& cam, bool first, bool last, float* out_rgb,
+                            uint8_t* out_rgb8, cudaStream_t s);
 
 // render.cu: full per-frame pipeline
 int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
@@ -228,6 +231,10 @@ void launch_fold(int64_t n, int shdim, double* pos, double* rot, double* scl, do
 
 CamDev make_cam(const gsv_camera& c);
 constexpr int kTile = 16;
+// per-tile state between depth-rank rounds (RenderWork::tile_done)
+constexpr uint8_t kTileOpen = 0;       // (C, T) of its pixels live in `state`
+constexpr uint8_t kTileSaturated = 1;  // every pixel T < 1e-4: written out, gets no more keys
+constexpr uint8_t kTileBlank = 2;      // no key yet: written out as background, state implied (0, 1)
 
 // ---- launch accounting and stage profiling (bench instrumentation) ---------
 extern long long g_launches;  // kernels launched by this library (all threads)

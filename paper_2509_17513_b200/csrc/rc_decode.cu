@@ -18,12 +18,16 @@
 // RAW-mode planes of these runs are first copied to 16-B aligned storage so
 // that every predictor plane is aligned.
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "gsv_internal.h"
 
 namespace gsv {
 
 constexpr int kRPW = 32;  // runs per warp
+
+// dev statistics: bytes redone on the careful path
+__device__ unsigned long long g_rc_slow_bytes;
 
 __global__ void copy_planes_kernel(const CopyJob* __restrict__ jobs, int njobs) {
     for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
@@ -135,6 +139,7 @@ __device__ __forceinline__ uint32_t adapt(uint32_t p, bool bit) {
 // quad 0 of tree Tn on exit.
 __device__ __forceinline__ uint32_t decode_byte_slow(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
                                                      uint32_t& code, CodedStream& cs) {
+    atomicAdd(&g_rc_slow_bytes, 1ull);
     uint32_t ctx = 1;
     uint32_t p = q0.y;  // node 1
     uint4 cq = q0;      // quad holding the children of ctx
@@ -164,52 +169,70 @@ __device__ __forceinline__ uint32_t decode_byte_slow(uint32_t T, uint32_t Tn, ui
     return ctx & 0xFFu;
 }
 
-// Fast path: the byte's decisions read the coded bits at a running offset
-// into the 64-bit buffer (one funnel shift) and defer the 8 probability
-// stores to the end of the byte, so a decision is: multiply, compare, select,
-// renormalise -- no buffer bookkeeping, no store, no branch.  It is exact as
-// long as the byte consumes at most 32 bits (>= 33 are buffered at the start);
-// otherwise nothing has been written and the byte is redone on the careful
-// path from the saved state.  Multi-byte samples alternate trees, so q0 of
-// the next tree is loaded during this byte; for one-byte samples the next
-// root quad is this tree's, patched in registers with the new node 1..3.
+// Fast path.  Within one byte the decisions only ever shift whole bytes in
+// (renormalisation by 8; a shift by 16 needs rng < 2^16 and is left to the
+// careful path), and the next four stream bytes sit in `bhi`, so the
+// renormalisation is a predicated byte permute of `code` with the next byte
+// and a predicated shift of `rng`; the next (rng >> 12) is selected from two
+// shifts computed beside the compare.  The bit-serial chain per decision is
+// then multiply -> compare -> select rng -> compare 2^24 -> select (rng >> 12).
+// The 8 probability stores are deferred to the end of the byte (so the
+// careful path can redo the byte from untouched state when it consumed more
+// than 4 bytes or needed a 16-bit shift: both are rare).  Multi-byte samples
+// alternate trees, so q0 of the next tree is loaded during this byte; for
+// one-byte samples the next root quad is this tree's, patched in registers.
+// a shift the compiler cannot fold into a select of shift amounts (which
+// would put the select before the shift on the serial chain)
+template <int S>
+__device__ __forceinline__ uint32_t shr_opaque(uint32_t x) {
+    uint32_t y;
+    asm("shr.b32 %0, %1, %2;" : "=r"(y) : "r"(x), "n"(S));
+    return y;
+}
+
 template <bool SAME_TREE>
 __device__ __forceinline__ uint32_t decode_byte(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
                                                 uint32_t& code, CodedStream& cs) {
     const uint32_t rng0 = rng, code0 = code;
-    const uint32_t bhi = (uint32_t)(cs.bb >> 32), blo = (uint32_t)cs.bb;
-    uint32_t ctx = 1, off = 0;
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);  // next 4 stream bytes, first in bits 31..24
+    uint32_t ctx = 1, sel = 0x2107u;               // byte_perm: (code << 8) | next stream byte
     uint32_t p = q0.y;
     uint4 cq = q0;
     uint4 qn = q0;
-    uint32_t pn[8];
+    uint32_t pn[8], na[8];
+    uint32_t a = rng >> 12;
+    bool wide = false;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         uint4 nq = make_uint4(0u, 0u, 0u, 0u);
         if (k < 6) nq = lds_quad(T + ctx * 16u);
         if (!SAME_TREE && k == 6) qn = lds_quad(Tn);
+        na[k] = node_addr(T, ctx);
         const uint32_t c0 = (ctx & 1) ? cq.z : cq.x;
         const uint32_t c1 = (ctx & 1) ? cq.w : cq.y;
-        const uint32_t bound = (rng >> 12) * p;
+        const uint32_t bound = a * p;
         const bool bit = code >= bound;
+        const uint32_t r = bit ? rng - bound : bound;
         code = bit ? code - bound : code;
-        rng = bit ? rng - bound : bound;
         pn[k] = adapt(p, bit);
         ctx = 2 * ctx + (bit ? 1u : 0u);
         p = bit ? c1 : c0;
         cq = nq;
-        const uint32_t sh = rng < (1u << 24) ? (rng < (1u << 16) ? 16u : 8u) : 0u;
-        code = __funnelshift_l(__funnelshift_lc(blo, bhi, off), code, sh);
-        rng <<= sh;
-        off += sh;
+        const bool lt24 = r < (1u << 24);
+        wide |= r < (1u << 16);
+        a = lt24 ? shr_opaque<4>(r) : shr_opaque<12>(r);  // both shifts beside the compare
+        rng = lt24 ? (r << 8) : r;
+        code = lt24 ? __byte_perm(code, bhi, sel) : code;
+        sel -= lt24 ? 1u : 0u;
     }
-    if (off > 32u) {  // rare: redo carefully (nothing was stored)
+    const uint32_t used = 0x2107u - sel;  // stream bytes shifted in
+    if (wide || used > 4u) {             // rare: redo carefully (nothing was stored)
         rng = rng0;
         code = code0;
         return decode_byte_slow(T, Tn, q0, rng, code, cs);
     }
 #pragma unroll
-    for (int k = 0; k < 8; k++) sts_u32(node_addr(T, ctx >> (8 - k)), pn[k]);
+    for (int k = 0; k < 8; k++) sts_u32(na[k], pn[k]);
     if (SAME_TREE) {
         const bool b0 = (ctx >> 7) & 1u;  // first decision: node 2 or 3 was updated second
         qn.y = pn[0];
@@ -217,13 +240,104 @@ __device__ __forceinline__ uint32_t decode_byte(uint32_t T, uint32_t Tn, uint4& 
         qn.w = b0 ? pn[1] : q0.w;
     }
     q0 = qn;
-    cs.bb <<= off;
-    cs.nbits -= (int32_t)off;
+    cs.bb <<= 8 * used;
+    cs.nbits -= (int32_t)(8 * used);
     cs.refill();
     return ctx & 0xFFu;
 }
 
-template <int NB, bool PREV>
+// Variant 2: the same fast path with the decision step written in PTX so
+// that the renormalisation, the code update and the node-address walk stay
+// predicated single instructions (the compiler otherwise expands selects into
+// two instructions).  Node addresses are walked directly: child = 2 * node -
+// T + 4 * bit (byte offsets, node n at T + 4n), grandchild quad at 4 * node -
+// 3T.
+template <bool SAME_TREE>
+__device__ __forceinline__ uint32_t decode_byte_v2(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
+                                                   uint32_t& code, CodedStream& cs) {
+    const uint32_t rng0 = rng, code0 = code;
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t sel = 0x2107u, rmin = 0xFFFFFFFFu;
+    uint32_t p = q0.y;
+    uint4 cq = q0;
+    uint4 qn = q0;
+    uint32_t pn[8], na[8];
+    uint32_t a = rng >> 12;
+    uint32_t node = T + 4u;                // node 1
+    const uint32_t m3T = 0u - 3u * T, c0T = 0u - T, c1T = 4u - T;
+    uint32_t pbit = 1u;                    // ctx & 1 of the current node (node 1: odd)
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+        if (k < 6) nq = lds_quad(4u * node + m3T);
+        if (!SAME_TREE && k == 6) qn = lds_quad(Tn);
+        na[k] = node;
+        const uint32_t c0 = pbit ? cq.z : cq.x;
+        const uint32_t c1 = pbit ? cq.w : cq.y;
+        uint32_t bitv, nnode;
+        asm("{\n\t"
+            ".reg .pred pb, pl;\n\t"
+            ".reg .u32 bnd, r1, r, t4, t12, K, d, off;\n\t"
+            "mul.lo.u32 bnd, %0, %9;\n\t"
+            "setp.ge.u32 pb, %2, bnd;\n\t"
+            "sub.u32 r1, %1, bnd;\n\t"
+            "selp.u32 r, r1, bnd, pb;\n\t"
+            "@pb sub.u32 %2, %2, bnd;\n\t"
+            "setp.lt.u32 pl, r, 16777216;\n\t"
+            "min.u32 %4, %4, r;\n\t"
+            "shr.u32 t4, r, 4;\n\t"
+            "shr.u32 t12, r, 12;\n\t"
+            "selp.u32 %0, t4, t12, pl;\n\t"
+            "@pl shl.b32 r, r, 8;\n\t"
+            "@pl prmt.b32 %2, %2, %10, %3;\n\t"
+            "@pl sub.u32 %3, %3, 1;\n\t"
+            "mov.u32 %1, r;\n\t"
+            "selp.u32 K, 15, 4096, pb;\n\t"
+            "sub.s32 d, K, %9;\n\t"
+            "shr.s32 d, d, 4;\n\t"
+            "add.u32 %5, %9, d;\n\t"
+            "selp.u32 %6, %12, %11, pb;\n\t"
+            "selp.u32 off, %14, %13, pb;\n\t"
+            "mad.lo.u32 %7, %15, 2, off;\n\t"
+            "selp.u32 %8, 1, 0, pb;\n\t"
+            "}"
+            : "+r"(a), "+r"(rng), "+r"(code), "+r"(sel), "+r"(rmin), "=r"(pn[k]), "=r"(p), "=r"(nnode),
+              "=r"(bitv)
+            : "r"(p), "r"(bhi), "r"(c0), "r"(c1), "r"(c0T), "r"(c1T), "r"(node));
+        node = nnode;
+        pbit = bitv;
+        cq = nq;
+    }
+    const uint32_t used = 0x2107u - sel;
+    if (rmin < (1u << 16) || used > 4u) {
+        rng = rng0;
+        code = code0;
+        return decode_byte_slow(T, Tn, q0, rng, code, cs);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) sts_u32(na[k], pn[k]);
+    const uint32_t ctx = (node - T) >> 2;  // 256 + byte value
+    if (SAME_TREE) {
+        const bool b0 = (ctx >> 7) & 1u;
+        qn.y = pn[0];
+        qn.z = b0 ? q0.z : pn[1];
+        qn.w = b0 ? pn[1] : q0.w;
+    }
+    q0 = qn;
+    cs.bb <<= 8 * used;
+    cs.nbits -= (int32_t)(8 * used);
+    cs.refill();
+    return ctx & 0xFFu;
+}
+
+template <int V, bool SAME_TREE>
+__device__ __forceinline__ uint32_t decode_byte_v(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
+                                                  uint32_t& code, CodedStream& cs) {
+    if constexpr (V == 2) return decode_byte_v2<SAME_TREE>(T, Tn, q0, rng, code, cs);
+    else return decode_byte<SAME_TREE>(T, Tn, q0, rng, code, cs);
+}
+
+template <int V, int NB, bool PREV>
 __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
                                              const uint32_t* __restrict__ prev,
                                              uint32_t* __restrict__ out, uint32_t hw, uint32_t w) {
@@ -236,53 +350,52 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
     cs.refill();
     uint32_t rng = 0xFFFFFFFFu;
     uint4 q0 = lds_quad(P);                  // root quad of tree 0
-    uint32_t pq0 = 0, pq1 = 0, pq2 = 0, pq3 = 0;  // previous-plane word queue
-    const uint32_t* pp = prev;
-    if (PREV) {
-        pq0 = pp[0];
-        pq1 = pp[1];
-        pq2 = pp[2];
-        pq3 = pp[3];
-        pp += 4;
-    }
+    // previous plane, 4 words at a time, one group ahead (planes are 16-B
+    // aligned with slack after them, so the read-ahead stays in bounds)
+    const uint4* pp = reinterpret_cast<const uint4*>(prev);
+    uint4 cur = make_uint4(0u, 0u, 0u, 0u), nxt = cur;
+    if (PREV) cur = __ldg(pp);
     uint32_t left = 0, above = 0, x = 0;
     const uint32_t nwords = (hw * NB + 3) / 4;
     uint32_t idx = 0;
-    for (uint32_t wi = 0; wi < nwords; wi++) {
-        uint32_t pw = 0;
-        if (PREV) {
-            pw = pq0;
-            pq0 = pq1;
-            pq1 = pq2;
-            pq2 = pq3;
-            pq3 = pp[0];
-            pp++;
-        }
-        uint32_t ow = 0;
-#pragma unroll
-        for (int j = 0; j < SPW; j++) {
-            if (SPW > 1 && idx >= hw) break;
-            uint32_t pred;
-            if (PREV) {
-                pred = (pw >> (8 * NB * j)) & mask;
-            } else {
-                pred = x > 0 ? left : (idx > 0 ? above : def);
+    for (uint32_t g = 0; g < nwords; g += 4) {
+        if (PREV) nxt = __ldg(pp + g / 4 + 1);
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {  // not unrolled: the loop body must stay small in the i-cache
+            const uint32_t wi = g + q;
+            if (wi >= nwords) break;
+            const uint32_t pw = q == 0 ? cur.x : (q == 1 ? cur.y : (q == 2 ? cur.z : cur.w));
+            uint32_t ow = 0, z = 0;
+            // one byte per iteration and a single inlined decoder instance,
+            // so the loop body stays small in the instruction cache
+#pragma unroll 1
+            for (int e = 0; e < SPW * NB; e++) {
+                const int j = e / NB, b = e % NB;
+                if (SPW > 1 && idx >= hw) break;
+                const uint32_t T = P + (uint32_t)b * kTreeBytes;
+                const uint32_t Tn = NB == 1 ? T : P + (uint32_t)((b + 1) % NB) * kTreeBytes;
+                z |= decode_byte_v<V, NB == 1>(T, Tn, q0, rng, code, cs) << (8 * b);
+                if (b == NB - 1) {
+                    uint32_t pred;
+                    if (PREV) {
+                        pred = (pw >> (8 * NB * j)) & mask;
+                    } else {
+                        pred = x > 0 ? left : (idx > 0 ? above : def);
+                    }
+                    const uint32_t v = (pred + ((z >> 1) ^ (0u - (z & 1u)))) & mask;  // unzigzag
+                    if (!PREV) {
+                        if (x == 0) above = v;
+                        left = v;
+                        if (++x == w) x = 0;
+                    }
+                    ow |= v << (8 * NB * j);
+                    idx++;
+                    z = 0;
+                }
             }
-            uint32_t z = 0;
-#pragma unroll
-            for (int b = 0; b < NB; b++)
-                z |= decode_byte<NB == 1>(P + b * kTreeBytes, P + ((b + 1) % NB) * kTreeBytes, q0, rng,
-                                          code, cs) << (8 * b);
-            const uint32_t v = (pred + ((z >> 1) ^ (0u - (z & 1u)))) & mask;  // unzigzag
-            if (!PREV) {
-                if (x == 0) above = v;
-                left = v;
-                if (++x == w) x = 0;
-            }
-            ow |= v << (8 * NB * j);
-            idx++;
+            out[wi] = ow;
         }
-        out[wi] = ow;
+        cur = nxt;
     }
 }
 
@@ -290,7 +403,7 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
 // behind each other): blocks [0, nb1) decode the 8-bit runs, the next nb2
 // blocks the 16-bit runs, the rest the 32-bit runs.  One warp per CTA, so
 // the warps land on separate SMs.
-template <int NB>
+template <int V, int NB>
 __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, const uint32_t* __restrict__ rc_runs,
                                             int n, int blk, const PlaneRef* __restrict__ planes, uint32_t P) {
     const int lane = threadIdx.x;
@@ -307,9 +420,9 @@ __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, co
         uint32_t* out = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(pr.samples));
         if (f > 0) {
             const uint32_t* prev = reinterpret_cast<const uint32_t*>(planes[r.plane_base + f - 1].samples);
-            decode_plane<NB, true>(P, pr, prev, out, hw, r.w);
+            decode_plane<V, NB, true>(P, pr, prev, out, hw, r.w);
         } else {
-            decode_plane<NB, false>(P, pr, nullptr, out, hw, r.w);
+            decode_plane<V, NB, false>(P, pr, nullptr, out, hw, r.w);
         }
     }
 }
@@ -320,6 +433,7 @@ struct RcClasses {
     int blk[4];  // block prefix
 };
 
+template <int V>
 __global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restrict__ runs,
                                                          const uint32_t* __restrict__ rc_runs, RcClasses c,
                                                          const PlaneRef* __restrict__ planes) {
@@ -327,9 +441,9 @@ __global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restri
     const int b = blockIdx.x;
     const int nb = b < c.blk[1] ? 1 : (b < c.blk[2] ? 2 : 4);
     const uint32_t P = (uint32_t)__cvta_generic_to_shared(probs_s) + threadIdx.x * lane_stride(nb);
-    if (b < c.blk[1]) decode_runs<1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P);
-    else if (b < c.blk[2]) decode_runs<2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P);
-    else decode_runs<4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P);
+    if (b < c.blk[1]) decode_runs<V, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P);
+    else if (b < c.blk[2]) decode_runs<V, 2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P);
+    else decode_runs<V, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P);
 }
 
 void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
@@ -346,8 +460,25 @@ void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n
     }
     if (c.blk[3] == 0) return;
     const size_t smem = (size_t)lane_stride(nbmax) * kRPW;
-    cudaFuncSetAttribute(rc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rc_decode_kernel<<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+    const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
+    const int v = ev ? atoi(ev) : 2;
+    if (v == 1) {
+        cudaFuncSetAttribute(rc_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rc_decode_kernel<1><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+    } else {
+        cudaFuncSetAttribute(rc_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rc_decode_kernel<2><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+    }
 }
 
 }  // namespace gsv
+
+extern "C" unsigned long long gsv_dev_rc_slow_bytes(int reset) {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, gsv::g_rc_slow_bytes, sizeof v);
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(gsv::g_rc_slow_bytes, &z, sizeof z);
+    }
+    return v;
+}

@@ -51,7 +51,15 @@ CamDev make_cam(const gsv_camera& c) {
 }
 
 // ---------------------------------------------------------------------------
-__global__ void reset_ctr_kernel(unsigned long long* ctr, long long n) {
+// Per-frame reset: counters, the radix digit histograms the producers of the
+// sort keys accumulate into (kHistRegions regions of 4 x 256), tile flags.
+constexpr int kHistRegions = 4;  // depth sort, tile sort of round 1, 2 (+1 spare)
+__global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ctr, long long n,
+                                                          uint32_t* __restrict__ ghist,
+                                                          uint8_t* __restrict__ tile_done, int ntiles) {
+    for (int i = threadIdx.x; i < kHistRegions * 1024; i += 256) ghist[i] = 0;
+    for (int i = threadIdx.x; i < ntiles; i += 256) tile_done[i] = 0;
+    if (threadIdx.x) return;
     ctr[C_NVIS] = 0;
     ctr[C_NKEYS] = 0;
     ctr[C_DMIN] = ~0ull;
@@ -70,26 +78,39 @@ __global__ void reset_ctr_kernel(unsigned long long* ctr, long long n) {
 // they sort last).  The radix sort runs on the top 32 significant bits of
 // that key (key32); full[] keeps the 64-bit key by splat index for the
 // fix-up of key32 ties.  Passes = bytes spanned by key32.
-__global__ void depth_key_prep(uint64_t* __restrict__ full, uint32_t* __restrict__ key32,
-                               unsigned long long* __restrict__ ctr) {
+// Also accumulates the digit histograms of all 4 radix passes (fused
+// radix_hist, sort.cuh).
+__global__ void __launch_bounds__(256) depth_key_prep(uint64_t* __restrict__ full, uint32_t* __restrict__ key32,
+                                                      unsigned long long* __restrict__ ctr,
+                                                      uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[4][256];
+#pragma unroll
+    for (int p = 0; p < 4; p++) h[p][threadIdx.x] = 0;
+    __syncthreads();
     const uint64_t n = ctr[C_N];
     const uint64_t nvis = ctr[C_NVIS];
     const uint64_t lo = ctr[C_DMIN], hi = ctr[C_DMAX];
     const uint64_t dead = nvis ? (hi - lo) + 1 : 0;
     const int bits = dead ? 64 - __clzll((long long)dead) : 0;
     const int shift = bits > 32 ? bits - 32 : 0;
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         const int kb = bits - shift;
         reinterpret_cast<int*>(ctr + C_NPASS)[0] = (nvis == 0 || (nvis == n && hi == lo)) ? 0 : (kb + 7) / 8;
         reinterpret_cast<int*>(ctr + C_NPASS)[1] = shift;
     }
-    if (i < n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = full[i];
         const uint64_t r = (k == ~0ull) ? dead : k - lo;
         full[i] = r;
-        key32[i] = (uint32_t)(r >> shift);
+        const uint32_t k32 = (uint32_t)(r >> shift);
+        key32[i] = k32;
+#pragma unroll
+        for (int p = 0; p < 4; p++) atomicAdd(&h[p][(k32 >> (8 * p)) & 0xFFu], 1u);
     }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
 }
 
 // Stable order among equal key32 values by the full key: one thread per run
@@ -167,8 +188,9 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
     const uint8_t* __restrict__ tile_done, uint32_t* __restrict__ tkey, uint32_t* __restrict__ tval,
     uint64_t cap, int ntx, unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
-    uint32_t epoch) {
+    uint32_t epoch, uint32_t* __restrict__ ghist, int tpasses) {
     __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_hist[4][256];
     __shared__ unsigned long long s_prefix;
     __shared__ uint32_t s_wsum[kEmitThreads / 32];
     if (threadIdx.x == 0) {
@@ -176,6 +198,8 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         if (t == gridDim.x - 1) *ticket = 0;  // every CTA has its ticket: reset for the next use
         s_tile = t;
     }
+#pragma unroll
+    for (int p = 0; p < 4; p++) s_hist[p][threadIdx.x] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t nvis = (uint32_t)ctr[C_NVIS];
@@ -201,7 +225,7 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
             const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
             uint32_t c = 0;
             for (uint32_t ty = y0; ty <= y1; ty++)
-                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] ? 0u : 1u;
+                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] == kTileSaturated ? 0u : 1u;
             cnt[k] = c;
         }
         sum += cnt[k];
@@ -264,14 +288,18 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         for (uint32_t ty = y0; ty <= y1; ty++)
             for (uint32_t tx = x0; tx <= x1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
-                if (tile_done[t]) continue;
+                if (tile_done[t] == kTileSaturated) continue;
                 if (o < cap) {
                     tkey[o] = t;
                     tval[o] = r;
+                    for (int p = 0; p < tpasses; p++) atomicAdd(&s_hist[p][(t >> (8 * p)) & 0xFFu], 1u);
                 }
                 o++;
             }
     }
+    __syncthreads();
+    for (int p = 0; p < tpasses; p++)
+        if (s_hist[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], s_hist[p][threadIdx.x]);
 }
 
 __global__ void tile_ranges(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ ctr,
@@ -303,7 +331,8 @@ void work_free(RenderWork* w) {
     free_ptr(w->state);
     free_ptr(w->tile_done);
     free_ptr(w->status);
-    free_ptr(w->hist);
+    free_ptr(w->sort_ghist);
+    free_ptr(w->sort_status);
     free_ptr(w->ctr);
     if (w->h_ctr) cudaFreeHost(w->h_ctr);
     *w = RenderWork();
@@ -361,15 +390,26 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         GSV_CUDA(cudaMalloc(&w->state, (size_t)npix * sizeof(float4)));
         w->cap_pix = npix;
     }
-    const int64_t hw = std::max(radix_hist_words(std::max(w->cap_n, w->cap_k)),
-                                scan_bsum_words(w->cap_n)) + 512;
-    if (hw > w->hist_cap) {
-        free_ptr(w->hist);
-        GSV_CUDA(cudaMalloc(&w->hist, hw * sizeof(uint32_t)));
-        w->hist_cap = hw;
+    if (!w->sort_ghist) {
+        GSV_CUDA(cudaMalloc(&w->sort_ghist, (kHistRegions * 1024 + 32) * sizeof(uint32_t)));
+        GSV_CUDA(cudaMemset(w->sort_ghist, 0, (kHistRegions * 1024 + 32) * sizeof(uint32_t)));
+    }
+    const int64_t sw = radix_status_words(std::max(w->cap_n, w->cap_k));
+    if (sw > w->sort_status_cap) {
+        free_ptr(w->sort_status);
+        GSV_CUDA(cudaMalloc(&w->sort_status, sw * sizeof(unsigned long long)));
+        GSV_CUDA(cudaMemset(w->sort_status, 0, sw * sizeof(unsigned long long)));
+        w->sort_status_cap = sw;
     }
     return GSV_OK;
 }
+
+static SortScratch sort_scratch(RenderWork* w) {
+    return SortScratch{w->sort_ghist, w->sort_status,
+                       reinterpret_cast<unsigned int*>(w->sort_ghist + kHistRegions * 1024), &w->sort_epoch};
+}
+
+static unsigned prep_grid(int64_t n) { return (unsigned)std::min<int64_t>((n + 1023) / 1024, 148 * 2); }
 
 static int tile_passes(int ntiles) {
     int bits = 0;
@@ -403,44 +443,42 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
-    uint32_t* digit_total = w->hist + (w->hist_cap - 512);
+    const SortScratch sc = sort_scratch(w);
     prof_mark(ST_PROJECT, s);
-    reset_ctr_kernel<<<1, 1, 0, s>>>(ctr, (long long)n);
+    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, w->tile_done, ntiles);
     project();
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
-        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr);
-        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, w->hist, digit_total, s);
+        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
+        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
-        count_launch(2 + 3 * 4);
+        count_launch(2 + radix_launches(4, true));
     }
     prof_mark(ST_EMIT, s);
     const unsigned g = 148 * 4;
     gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
-    launch_state_init(w->state, w->tile_done, (size_t)npix, ntiles, s);
-    count_launch(2);
+    count_launch(1);
     std::vector<uint32_t> bounds;
     round_bounds(n, &bounds);
     const int tp = tile_passes(ntiles);
     for (size_t j = 0; j + 1 < bounds.size(); j++) {
         const uint32_t a = bounds[j], b = bounds[j + 1];
         prof_mark(ST_EMIT, s);
-        const unsigned ge = (unsigned)((b - a + kEmitTile - 1) / kEmitTile);
+        const unsigned ge = std::max(1u, (unsigned)((b - a + kEmitTile - 1) / kEmitTile));
+        uint32_t* th = sc.ghist + 1024 * (1 + (int)std::min<size_t>(j, kHistRegions - 2));
         round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b, w->tile_done, w->tkey[0],
                                                       w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
-                                                      w->ticket, ++w->epoch);
+                                                      w->ticket, ++w->epoch, th, tp);
         count_launch(1);
         prof_mark(ST_TSORT, s);
-        radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, w->hist, digit_total, s);
-        count_launch(3 * tp);
+        radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
+        count_launch(radix_launches(tp, true));
         prof_mark(ST_COMPOSITE, s);
         launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
-                               w->tile_done, cam, s);
+                               w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
         count_launch(1);
     }
-    launch_finalize(w->state, cam, out_rgb, out_rgb8, s);
-    count_launch(1);
     prof_mark(ST_COUNT, s);
     cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     GSV_CUDA(cudaGetLastError());
@@ -511,12 +549,12 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
-    uint32_t* digit_total = w->hist + (w->hist_cap - 512);
-    reset_ctr_kernel<<<1, 1, 0, s>>>(ctr, (long long)n);
+    const SortScratch sc = sort_scratch(w);
+    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, w->tile_done, 0);
     launch_project_soa(src, cam, w, rects, depth, s);
     if (n > 0) {
-        depth_key_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr);
-        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, w->hist, digit_total, s);
+        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
+        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         copy_order<<<148 * 4, 256, 0, s>>>(w->didx[0], w->didx[1], ctr, order, w->rec, tile_count);
     }
