@@ -258,10 +258,14 @@ def run_b200(a, rank, world, dist):
         e2e = {"value": round(f, 2), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(a.frames * a.width * a.height * 3)}
 
-    # roofline of the dominant stage
+    # roofline of the dominant stage (CUDA events around its launches on the
+    # launching stream, one single-stream step)
     stage_ms = {k: v["ms"] for k, v in prof.items()}
     dom = max(stage_ms, key=stage_ms.get)
-    roof = roofline(a, blobs[a.codec], dom, prof, st0)
+    roof = roofline(a, blobs[a.codec], dom, prof, st0, a.evals_per_frame)
+    frame_bytes = (len(blobs[a.codec]) / a.frames
+                   + sum(stage_bytes(a, blobs[a.codec], k, st0) / a.frames
+                         for k in ("project", "depth_sort", "key_emit", "tile_sort", "composite")))
     result = {
         "metric": METRIC, "value": round(fps, 2), "unit": "frames/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 3),
@@ -278,37 +282,89 @@ def run_b200(a, rank, world, dist):
         "roofline": roof, "stages_ms_per_frame": {k: round(v["ms"] / a.frames, 5)
                                                   for k, v in prof.items()},
         "render_stats": st0, "per_layer": sweep,
+        # whole-frame HBM roofline: algorithmic bytes of one
+        # decoded+rendered frame x fps against the HBM peak
+        "frame_roofline": {"bytes_per_frame": int(frame_bytes),
+                           "achieved_gbs": round(frame_bytes * fps / 1e9, 1),
+                           "peak_gbs": peaks()[0], "frac": round(frame_bytes * fps / 1e9 / peaks()[0], 4)},
     }
     return result
 
 
 def stage_bytes(a, blob, stage, st):
-    """Algorithmic bytes of one step for a stage."""
-    n, nvis, K = st["n_splats"], st["n_visible"], st["n_keys"]
+    """Algorithmic HBM bytes of one step for a stage:
+    what the stage must move at minimum, per frame x frames."""
+    n, nvis = st["n_splats"], st["n_visible"]
+    k_emit = st["n_keys_emitted"]
     npx = a.width * a.height
     per_frame = {
-        "project": 26 * n + 8 * n + 4 * n + 48 * nvis,        # codes in, key+idx+record out
-        "depth_sort": 7 * (2 * 12 * n),                          # 7 passes, read+write key+idx
-        "key_emit": 48 * 2 * nvis + 8 * nvis + 8 * K,           # gather records, counts, keys out
-        "tile_sort": 2 * (2 * 8 * K),                            # 2 passes, read+write key+val
-        "tile_ranges": 4 * K,
-        "composite": 4 * K + 48 * K + 12 * npx,                  # ranks, records, image
+        # codes in (26 B/splat at SH degree 1), depth key + index + 64-B record out
+        "project": 26 * n + 12 * n + 64 * nvis,
+        # 4 passes: read + write (4-B key, 4-B index)
+        "depth_sort": 4 * 2 * 8 * n,
+        # gather (index + record in, record out) and key emission (record in, key out)
+        "key_emit": (4 + 64 + 64) * nvis + 64 * nvis + 8 * k_emit,
+        # 2 passes over the emitted (tile, rank) keys
+        "tile_sort": 2 * 2 * 8 * k_emit,
+        "tile_ranges": 0,
+        # per emitted key: rank + 48 B of the record used; the fp32 image out
+        "composite": (4 + 48) * k_emit + 12 * npx,
     }
     if stage in per_frame:
         return per_frame[stage] * a.frames
     return len(blob)  # decode stages: the container bytes read once per step
 
 
-def roofline(a, blob, stage, prof, st):
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md: MEASURED_PEAKS.json absent)"
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture summary (profiles/ncu_traffic.json)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(kernel)
+
+
+KERNEL_OF = {"composite": "composite_strip_kernel", "project": "project_kernel",
+             "depth_sort": "radix_onesweep", "tile_sort": "radix_onesweep",
+             "key_emit": "round_emit_fused", "range_decode": "rc_decode_kernel", "crc": "crc_kernel"}
+MUFU_EX2_PER_CLK_SM = 16          # B200 SFU rate (ex2.approx), per SM per clock
+SMS, SM_MHZ_MAX = 148, 1965.0
+
+
+def roofline(a, blob, stage, prof, st, evals_per_frame):
+    peak, src = peaks()
     ms = prof[stage]["ms"]
+    launches = int(prof[stage].get("intervals", 0))
     b = stage_bytes(a, blob, stage, st)
     achieved = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-    return {"bound": "hbm", "kernel": stage, "achieved": round(achieved, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-            "algorithmic_bytes_per_step": int(b), "ms_per_step": round(ms, 3)}
+    tr = ncu_traffic(KERNEL_OF.get(stage, stage))
+    out = {"bound": "hbm", "kernel": KERNEL_OF.get(stage, stage), "stage": stage,
+           "achieved": round(achieved, 1), "peak": peak, "peak_source": src, "unit": "GB/s",
+           "frac": round(achieved / peak, 4),
+           "traffic": tr["dram_bytes_per_launch"] if tr else None,
+           "traffic_source": tr["source"] if tr else None,
+           "algorithmic_bytes_per_step": int(b), "ms_per_step": round(ms, 3),
+           "launches_per_step": launches}
+    if stage == "composite" and evals_per_frame:
+        # the compositor is issue-bound, not HBM-bound: every pixel evaluation
+        # needs one ex2 on the SFU, the scarcest pipe it uses
+        ev = evals_per_frame * a.frames / (ms / 1e3)
+        pk = MUFU_EX2_PER_CLK_SM * SMS * SM_MHZ_MAX * 1e6
+        out["compute"] = {"unit": "pixel-evals/s", "achieved": round(ev, 1),
+                          "peak": pk, "peak_basis": "SFU ex2: 16/clk/SM x 148 SMs x 1965 MHz",
+                          "frac": round(ev / pk, 4),
+                          "evals_per_frame": int(evals_per_frame),
+                          "evals_source": "CPU oracle composite of frame 0 (same splats, same order)"}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -338,8 +394,23 @@ def cpu_reference(a, threads, samples, rank_seed=1002):
                                        f"{a.width}x{a.height}, {threads} threads"}
 
 
+def oracle_evals(a, rank_seed=1002):
+    """Pixel evaluations (in-rect, T >= 1e-4) of frame 0 by the CPU oracle:
+    the useful work of the compositor, for its compute roofline."""
+    from oracle import oracle as O
+    blobs, _ = make_inputs(a, rank_seed)
+    data = blobs[a.codec]
+    info = O.read_structure(data)
+    vals = O.decode_group_codes(data, info, 0, a.k)
+    f0 = O.assemble(info, info.groups[0], vals, a.k)[0]
+    means, covs, depth, colors, opac, rects, _ = O.project_set(f0, camera(a))
+    _, ev = O.composite(means, covs, depth, colors, opac, rects, camera(a), want_evals=True)
+    return ev
+
+
 def main():
     a = parse()
+    a.evals_per_frame = None
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     dist = None
@@ -371,6 +442,11 @@ def main():
         if dist:
             dist.destroy_process_group()
         return
+    if rank == 0 and not a.no_cpu:
+        try:
+            a.evals_per_frame = oracle_evals(a)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] oracle eval count unavailable: {e}", file=sys.stderr)
     res = run_b200(a, rank, world, dist)
     if rank == 0:
         if not a.no_cpu:

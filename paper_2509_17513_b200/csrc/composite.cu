@@ -29,6 +29,26 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__
     return lo;
 }
 
+// Same with the whole warp: 32 probes per step (about log32(n) dependent
+// loads instead of log2(n)); every lane returns the result.
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* __restrict__ k, uint32_t n, uint32_t t) {
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + (uint32_t)lane * step;
+        const bool lt = p < hi && __ldg(k + p) < t;
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, lt));  // probes below t
+        if (c == 0) return lo;
+        const uint32_t nlo = lo + (c - 1) * step + 1;
+        hi = min(hi, lo + c * step);
+        lo = nlo;
+    }
+    const uint32_t p = lo + (uint32_t)lane;
+    const bool lt = p < hi && __ldg(k + p) < t;
+    return lo + __popc(__ballot_sync(0xffffffffu, lt));
+}
+
 __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
@@ -53,19 +73,21 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
     uint8_t* __restrict__ out_rgb8) {
-    constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile; a CTA of 4 warps holds 4/kStrips tiles
+    constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
     __shared__ __align__(16) float4 s_rec[4][32 * 4];
-    __shared__ int s_unsat[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw = blockIdx.x * 4 + warp;
     const int tile = gw / kStrips, strip = gw % kStrips;
-    // saturated tiles were written out in an earlier round; blank ones too,
-    // unless this round brings them keys
-    const uint8_t td = (tile < ntiles && !first) ? tile_done[tile] : kTileOpen;
-    bool on = tile < ntiles && td != kTileSaturated;
-    uint32_t bound = 0;
-    if (on && lane < 2) bound = lower_bound_u32(keys, (uint32_t)*nkeys, (uint32_t)tile + lane);
-    const uint32_t start = __shfl_sync(0xffffffffu, bound, 0), end = __shfl_sync(0xffffffffu, bound, 1);
+    if (tile >= ntiles) return;
+    // per-strip state: saturated strips were written out in an earlier round;
+    // blank ones too, unless this round brings their tile keys
+    uint8_t* flag = tile_done + 4 * (size_t)tile + strip;
+    const uint8_t td = first ? kTileOpen : *flag;
+    if (td == kTileSaturated) return;
+    const uint32_t K = (uint32_t)*nkeys;
+    const uint32_t start = warp_lower_bound(keys, K, (uint32_t)tile);
+    const uint32_t end = warp_lower_bound(keys, K, (uint32_t)tile + 1);
+    bool on = true;
     const int tx = on ? tile % ntx : 0, ty = on ? tile / ntx : 0;
     const int px = tx * kTile + (lane & 15);
     const int sy0 = ty * kTile + strip * 2 * ROWS;  // strip's first row
@@ -110,48 +132,50 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             const float4 rc = lds_f4(ra);  // x0, y0, x1, y1 (exact integers)
             // strip rows [sy0, sy0 + 2 ROWS) against [y0, y1): warp-uniform skip
             if (rc.y >= (float)(sy0 + 2 * ROWS) || rc.w <= (float)sy0) continue;
-            if (pxf < rc.x || pxf >= rc.z) continue;  // column outside the rect
+            // rows of the lane's column inside the rect (empty outside its columns)
+            const bool colin = pxf >= rc.x && pxf < rc.z;
             const int lo = min(max((int)rc.y - py0, 0), ROWS), hi = min(max((int)rc.w - py0, 0), ROWS);
-            const uint32_t m = ((0xFFFFu << lo) & ~(0xFFFFu << hi)) & live;
-            if (!m) continue;
+            const uint32_t m = colin ? ((0xFFFFu << lo) & ~(0xFFFFu << hi)) : 0u;
+            if (!__any_sync(0xffffffffu, m & live)) continue;  // converged: lanes mask, not branch
             const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
             const float op = lds_f4(ra + 48u).x;
             const float dx = (pxf - rc.x) - a.x;
             const float A = a.z * dx * dx, B = a.w * dx;
             const float dy0 = (py0f - rc.y) - a.y;
-            // branch-free over the lane's rows (masked rows get alpha 0, which
-            // leaves C and T bit-identical), so the ROWS chains interleave
-            uint32_t dead = 0;
+            // branch-free over the lane's rows: a pixel outside the rect or
+            // already at T < 1e-4 gets alpha 0, and alpha <= 0 composites as a
+            // no-op (C, T unchanged), so the ROWS chains interleave
 #pragma unroll
             for (int j = 0; j < ROWS; j++) {
                 const float dy = dy0 + (float)j;
                 const float pw = fminf(fmaf(fmaf(b.x, dy, B), dy, A), 0.0f);
                 float e;
                 asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw));
-                float alpha = fminf(op * e, 0.99f);
-                alpha = ((m >> j) & 1u) && alpha > 0.0f ? alpha : 0.0f;
+                const float al = fminf(fmaxf(op * e, 0.0f), 0.99f);
+                float alpha;  // row bit of m and T >= 1e-4, as one bit test + one compare
+                asm("{\n\t.reg .pred pm, pt;\n\t.reg .b32 t;\n\t"
+                    "and.b32 t, %1, %2;\n\tsetp.ne.b32 pm, t, 0;\n\t"
+                    "setp.ge.and.f32 pt, %3, 0f38D1B717, pm;\n\t"
+                    "selp.f32 %0, %4, 0f00000000, pt;\n\t}"
+                    : "=f"(alpha) : "r"(m), "r"(1u << j), "f"(T[j]), "f"(al));
                 const float w = T[j] * alpha;
                 c0[j] = fmaf(w, b.y, c0[j]);
                 c1[j] = fmaf(w, b.z, c1[j]);
                 c2[j] = fmaf(w, b.w, c2[j]);
-                T[j] = T[j] * (1.0f - alpha);
-                dead |= (T[j] < 1e-4f ? 1u : 0u) << j;
+                T[j] = T[j] - w;  // T (1 - alpha)
             }
-            live &= ~dead;
         }
+        // live pixels for the early exit and the skip test, once per batch
+        live = 0;
+#pragma unroll
+        for (int j = 0; j < ROWS; j++) live |= (T[j] >= 1e-4f ? 1u : 0u) << j;
+        live &= inimg;
         __syncwarp();
     }
-    const bool wsat = __all_sync(0xffffffffu, (live & inimg) == 0);
-    bool tsat = wsat;
-    if constexpr (kStrips > 1) {
-        if (lane == 0) s_unsat[warp] = wsat ? 0 : 1;
-        __syncthreads();
-        const int w0 = warp - strip;
-        for (int k = 0; k < kStrips; k++) tsat = tsat && s_unsat[w0 + k] == 0;
-    }
+    const bool tsat = __all_sync(0xffffffffu, (live & inimg) == 0);
     if (!on) return;
-    // finish the tile (background blend, clip: render.py:333-338, 356) when
+    // finish the strip (background blend, clip: render.py:333-338, 356) when
     // it saturated, in the last round, and as blank background when the first
     // round brought it no key; otherwise carry (C, T) to the next round
     const bool blank = first && !work && !last;
@@ -168,17 +192,17 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
                 if (out_rgb8) out_rgb8[3 * pix + k] = (uint8_t)floorf(x * 255.0f + 0.5f);
             }
         }
-        if (strip == 0 && lane == 0 && !last) tile_done[tile] = tsat ? kTileSaturated : kTileBlank;
+        if (lane == 0 && !last) *flag = tsat ? kTileSaturated : kTileBlank;
     } else if (work) {
 #pragma unroll
         for (int j = 0; j < ROWS; j++)
             if ((inimg >> j) & 1u)
                 state[(size_t)(py0 + j) * width + px] = make_float4(c0[j], c1[j], c2[j], T[j]);
-        if (strip == 0 && lane == 0 && td != kTileOpen) tile_done[tile] = kTileOpen;
+        if (lane == 0 && td != kTileOpen) *flag = kTileOpen;
     }
 }
 
-static int composite_rows() {
+int composite_rows() {
     static int rows = 0;
     if (!rows) {
         const char* e = getenv("GSV_COMPOSITE_ROWS");

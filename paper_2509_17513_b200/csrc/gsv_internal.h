@@ -212,6 +212,7 @@ void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
 // One depth-rank round; `first` starts from (C, T) = (0, 1), `last` writes the
 // final image of every tile still open (saturated tiles are written when they
 // saturate).
+int composite_rows();  // pixel rows per lane of the compositor (GSV_COMPOSITE_ROWS: 2, 4, 8)
 void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
                             const unsigned long long* nkeys, const SplatRec* recs, float4* state,
                             uint8_t* tile_done, const CamDev& cam, bool first, bool last, float* out_rgb,
@@ -231,10 +232,13 @@ void launch_fold(int64_t n, int shdim, double* pos, double* rot, double* scl, do
 
 CamDev make_cam(const gsv_camera& c);
 constexpr int kTile = 16;
-// per-tile state between depth-rank rounds (RenderWork::tile_done)
+// per-strip state between depth-rank rounds (RenderWork::tile_done: 4 bytes
+// per tile, one per strip of the compositor; bytes past the strip count are
+// kTileSaturated, so a tile is saturated iff its word is 0x01010101)
 constexpr uint8_t kTileOpen = 0;       // (C, T) of its pixels live in `state`
 constexpr uint8_t kTileSaturated = 1;  // every pixel T < 1e-4: written out, gets no more keys
-constexpr uint8_t kTileBlank = 2;      // no key yet: written out as background, state implied (0, 1)
+constexpr uint8_t kTileBlank = 2;
+constexpr uint32_t kTileAllSat = 0x01010101u;      // no key yet: written out as background, state implied (0, 1)
 
 // ---- launch accounting and stage profiling (bench instrumentation) ---------
 extern long long g_launches;  // kernels launched by this library (all threads)

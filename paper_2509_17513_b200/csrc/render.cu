@@ -56,9 +56,10 @@ CamDev make_cam(const gsv_camera& c) {
 constexpr int kHistRegions = 4;  // depth sort, tile sort of round 1, 2 (+1 spare)
 __global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ctr, long long n,
                                                           uint32_t* __restrict__ ghist,
-                                                          uint8_t* __restrict__ tile_done, int ntiles) {
+                                                          uint32_t* __restrict__ tile_done, int ntiles,
+                                                          uint32_t open_word) {
     for (int i = threadIdx.x; i < kHistRegions * 1024; i += 256) ghist[i] = 0;
-    for (int i = threadIdx.x; i < ntiles; i += 256) tile_done[i] = 0;
+    for (int i = threadIdx.x; i < ntiles; i += 256) tile_done[i] = open_word;
     if (threadIdx.x) return;
     ctr[C_NVIS] = 0;
     ctr[C_NKEYS] = 0;
@@ -180,13 +181,19 @@ __global__ void gather_sorted(const SplatRec* __restrict__ rec, SplatRec* __rest
 // emit.
 constexpr int kEmitThreads = 256, kEmitPer = 1, kEmitTile = kEmitThreads * kEmitPer;
 
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long st_pack(uint32_t epoch, uint32_t flag, unsigned long long v) {
     return ((unsigned long long)(epoch & 0xFFFFFFu) << 40) | ((unsigned long long)flag << 38) | v;
 }
 
 __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
-    const uint8_t* __restrict__ tile_done, uint32_t* __restrict__ tkey, uint32_t* __restrict__ tval,
+    const uint32_t* __restrict__ tile_done, uint32_t* __restrict__ tkey, uint32_t* __restrict__ tval,
     uint64_t cap, int ntx, unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
     uint32_t epoch, uint32_t* __restrict__ ghist, int tpasses) {
     __shared__ uint32_t s_tile;
@@ -225,7 +232,7 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
             const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
             uint32_t c = 0;
             for (uint32_t ty = y0; ty <= y1; ty++)
-                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] == kTileSaturated ? 0u : 1u;
+                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] == kTileAllSat ? 0u : 1u;
             cnt[k] = c;
         }
         sum += cnt[k];
@@ -246,28 +253,39 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         total += s_wsum[w];
     }
     const uint32_t excl = wb + x - sum;
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
+        // decoupled look-back, 32 predecessors per step (one per lane)
         unsigned long long prefix = 0;
         if (tile == 0) {
-            atomicExch(status, st_pack(epoch, 2, total));
+            if (lane == 0) atomicExch(status, st_pack(epoch, 2, total));
         } else {
-            atomicExch(status + tile, st_pack(epoch, 1, total));
+            if (lane == 0) atomicExch(status + tile, st_pack(epoch, 1, total));
+            const uint32_t ep = epoch & 0xFFFFFFu;
             int j = (int)tile - 1;
             for (;;) {
-                const unsigned long long wv = atomicAdd(status + j, 0ull);
-                const uint32_t ep = (uint32_t)(wv >> 40), fl = (uint32_t)(wv >> 38) & 3u;
-                if (ep != (epoch & 0xFFFFFFu) || fl == 0) {
-                    __nanosleep(32);
-                    continue;
-                }
-                prefix += wv & ((1ull << 38) - 1);
-                if (fl == 2) break;
-                j--;
+                const int idx = j - lane;
+                const unsigned long long wv = idx >= 0 ? ld_volatile_u64(status + idx) : st_pack(epoch, 2, 0);
+                const uint32_t fl = (uint32_t)(wv >> 38) & 3u;
+                const bool valid = (uint32_t)(wv >> 40) == ep && fl != 0;
+                const uint32_t inv = __ballot_sync(0xffffffffu, !valid);
+                const uint32_t inc = __ballot_sync(0xffffffffu, valid && fl == 2);
+                // lanes [0, k) are consumed this step
+                const uint32_t first_inv = inv ? (uint32_t)(__ffs(inv) - 1) : 32u;
+                const uint32_t first_inc = inc ? (uint32_t)(__ffs(inc) - 1) : 32u;
+                const bool done = first_inc < first_inv;
+                const uint32_t k = done ? first_inc + 1 : first_inv;
+                unsigned long long v = (uint32_t)lane < k ? (wv & ((1ull << 38) - 1)) : 0ull;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (done) break;
+                j -= (int)k;
+                if (k == 0) __nanosleep(32);
             }
-            atomicExch(status + tile, st_pack(epoch, 2, prefix + total));
+            if (lane == 0) atomicExch(status + tile, st_pack(epoch, 2, prefix + total));
         }
-        s_prefix = prefix;
-        if (tile == nt - 1) {
+        if (lane == 0) s_prefix = prefix;
+        if (lane == 0 && tile == nt - 1) {
             const unsigned long long K = prefix + total;
             ctr[C_NKEYS] = K;
             ctr[C_KCLAMP] = K < cap ? K : cap;
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         for (uint32_t ty = y0; ty <= y1; ty++)
             for (uint32_t tx = x0; tx <= x1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
-                if (tile_done[t] == kTileSaturated) continue;
+                if (tile_done[t] == kTileAllSat) continue;
                 if (o < cap) {
                     tkey[o] = t;
                     tval[o] = r;
@@ -382,7 +400,7 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         free_ptr(w->range);
         free_ptr(w->tile_done);
         GSV_CUDA(cudaMalloc(&w->range, (size_t)tiles * 2 * sizeof(uint32_t)));
-        GSV_CUDA(cudaMalloc(&w->tile_done, (size_t)tiles));
+        GSV_CUDA(cudaMalloc(&w->tile_done, (size_t)tiles * 4));
         w->cap_tiles = tiles;
     }
     if (npix > w->cap_pix) {
@@ -407,6 +425,14 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
 static SortScratch sort_scratch(RenderWork* w) {
     return SortScratch{w->sort_ghist, w->sort_status,
                        reinterpret_cast<unsigned int*>(w->sort_ghist + kHistRegions * 1024), &w->sort_epoch};
+}
+
+// the tile_done word of a fresh tile: its strips open, the unused bytes saturated
+static uint32_t open_word(int rows) {
+    const int strips = 16 / (2 * rows);
+    uint32_t w = 0;
+    for (int k = strips; k < 4; k++) w |= (uint32_t)kTileSaturated << (8 * k);
+    return w;
 }
 
 static unsigned prep_grid(int64_t n) { return (unsigned)std::min<int64_t>((n + 1023) / 1024, 148 * 2); }
@@ -445,7 +471,8 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
     const SortScratch sc = sort_scratch(w);
     prof_mark(ST_PROJECT, s);
-    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, w->tile_done, ntiles);
+    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, reinterpret_cast<uint32_t*>(w->tile_done),
+                                          ntiles, open_word(composite_rows()));
     project();
     count_launch(2);
     prof_mark(ST_DSORT, s);
@@ -467,7 +494,8 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         prof_mark(ST_EMIT, s);
         const unsigned ge = std::max(1u, (unsigned)((b - a + kEmitTile - 1) / kEmitTile));
         uint32_t* th = sc.ghist + 1024 * (1 + (int)std::min<size_t>(j, kHistRegions - 2));
-        round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b, w->tile_done, w->tkey[0],
+        round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b,
+                                                      reinterpret_cast<const uint32_t*>(w->tile_done), w->tkey[0],
                                                       w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
                                                       w->ticket, ++w->epoch, th, tp);
         count_launch(1);
@@ -550,7 +578,8 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
     unsigned long long* ctr = w->ctr;
     int* npass = reinterpret_cast<int*>(ctr + C_NPASS);
     const SortScratch sc = sort_scratch(w);
-    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, w->tile_done, 0);
+    reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, reinterpret_cast<uint32_t*>(w->tile_done), 0,
+                                          0u);
     launch_project_soa(src, cam, w, rects, depth, s);
     if (n > 0) {
         depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);

@@ -8,6 +8,6 @@ for k in $ks; do
     rc_decode_kernel) cod=1; cnt=2;;
     *) cod=0; cnt=2;;
   esac
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c $cnt \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s ${SKIP:-2} -c $cnt \
      -o gpurun_out/${tag}_$k python tools/ncu_driver.py $cod > gpurun_out/${tag}_$k.log 2>&1
 done
