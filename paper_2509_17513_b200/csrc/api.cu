@@ -13,6 +13,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,19 +41,61 @@ struct gsv_session {
 
 namespace {
 
+// Device blocks are recycled through a process-wide pool: opening a
+// container and its descriptor uploads would otherwise cudaMalloc/cudaFree
+// (both synchronising) on every call.  A block goes back to the pool when its
+// owner is destroyed -- gsv_video_close synchronises the session first, so no
+// kernel still uses it -- and is reused for a request of at most its size
+// and at least half of it.  The pool is emptied when cudaMalloc fails.
+std::mutex g_pool_mu;
+std::multimap<size_t, void*> g_pool;  // capacity -> block
+
+void pool_put(void* p, size_t cap) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.emplace(cap, p);
+}
+
+void* pool_get(size_t bytes, size_t* cap) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto it = g_pool.lower_bound(bytes);
+        if (it != g_pool.end() && it->first <= 2 * bytes + (1u << 20)) {
+            void* p = it->second;
+            *cap = it->first;
+            g_pool.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (auto& kv : g_pool) cudaFree(kv.second);
+        g_pool.clear();
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    }
+    *cap = bytes;
+    return p;
+}
+
 struct DevBuf {
     void* p = nullptr;
-    size_t n = 0;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
+    size_t n = 0;    // bytes requested
+    size_t cap = 0;  // bytes of the block
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { pool_put(p, cap); }
     int alloc(size_t bytes) {
-        if (p) cudaFree(p);
-        p = nullptr;
         n = bytes;
+        if (p && bytes <= cap) return GSV_OK;
+        pool_put(p, cap);
+        p = nullptr;
+        cap = 0;
         if (bytes == 0) return GSV_OK;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return fail(GSV_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        p = pool_get(bytes, &cap);
+        if (!p) return fail(GSV_E_CUDA, "cudaMalloc: out of memory");
         return GSV_OK;
     }
     template <class T>

@@ -206,8 +206,8 @@ int composite_rows() {
     static int rows = 0;
     if (!rows) {
         const char* e = getenv("GSV_COMPOSITE_ROWS");
-        rows = e ? atoi(e) : 4;
-        if (rows != 2 && rows != 4 && rows != 8) rows = 4;
+        rows = e ? atoi(e) : 8;
+        if (rows != 2 && rows != 4 && rows != 8) rows = 8;
     }
     return rows;
 }

@@ -66,21 +66,59 @@ struct SplatIn {
     double sh[SHD];
 };
 
+// Samples of one slot: 16-bit samples are read with one aligned 16-bit load
+// when the plane is 2-B aligned (codec-0 planes are consumed in place and
+// may not be).
+__device__ __forceinline__ uint32_t load_sample_fast(const uint8_t* p, uint32_t j, int bits) {
+    if (bits == 8) return __ldg(p + j);
+    if (bits == 16) {
+        const uint8_t* q = p + 2 * (size_t)j;
+        if ((reinterpret_cast<uintptr_t>(p) & 1u) == 0)
+            return __ldg(reinterpret_cast<const uint16_t*>(q));
+        return (uint32_t)__ldg(q) | ((uint32_t)__ldg(q + 1) << 8);
+    }
+    return load_sample_p(p, j, bits);
+}
+
+// Per block: the frame's slot descriptors and the 8-bit quotient table live in
+// shared memory (stage() in the kernel prologue), so a slot costs one LDS
+// for its descriptor and one global load for its code; all of a splat's
+// codes are loaded before any is dequantized.
 struct PlaneLoader {
     FrameSrc src;
     __device__ __forceinline__ int64_t count() const { return src.layer_off[src.nlayers]; }
+    static size_t smem_bytes(const FrameSrc& f) { return 256 * sizeof(double) + (size_t)f.nlayers * f.nslots * sizeof(SlotDesc); }
+    __device__ __forceinline__ void stage(unsigned char* smem) const {
+        double* q8 = reinterpret_cast<double*>(smem);
+        SlotDesc* sd = reinterpret_cast<SlotDesc*>(smem + 256 * sizeof(double));
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) q8[k] = g_q8[k];
+        const int nsd = src.nlayers * src.nslots;
+        for (int k = threadIdx.x; k < nsd; k += blockDim.x) sd[k] = src.slots[k];
+        __syncthreads();
+    }
+    __device__ __forceinline__ double deq(uint32_t code, const SlotDesc& d, const double* s_q8) const {
+        double q;
+        if (d.dir_bits == 8 && code < 256u) q = s_q8[code];
+        else if (d.dir_bits == 16 && code < 65536u) q = __ldg(g_q16 + code);
+        else q = __ddiv_rn((double)code, d.dir_bits >= 32 ? 4294967295.0 : (double)((1ull << d.dir_bits) - 1ull));
+        return __dadd_rn(d.rmin, __dmul_rn(q, d.span));
+    }
     // slots [S0, S1): geometry (0..10) first, SH (11..) only for survivors,
     // which keeps the SH registers out of the projection's live range
     template <int DEG, int S0, int S1>
-    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a) const {
+    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a, const unsigned char* smem) const {
+        const double* s_q8 = reinterpret_cast<const double*>(smem);
+        const SlotDesc* s_sd = reinterpret_cast<const SlotDesc*>(smem + 256 * sizeof(double));
         int l = 0;
         while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
         const uint32_t j = i - src.layer_off[l];
-        const SlotDesc* sd = src.slots + (size_t)l * src.nslots;
+        const SlotDesc* sd = s_sd + (size_t)l * src.nslots;
+        uint32_t code[S1 - S0];
+#pragma unroll
+        for (int s = S0; s < S1; s++) code[s - S0] = load_sample_fast(sd[s].samples, j, sd[s].bits);
 #pragma unroll
         for (int s = S0; s < S1; s++) {
-            const SlotDesc d = sd[s];
-            const double v = dequant_p(load_sample_p(d.samples, j, d.bits), d);
+            const double v = deq(code[s - S0], sd[s], s_q8);
             if (s < 3) a.p[s] = v;
             else if (s < 7) a.q[s - 3] = v;
             else if (s < 10) a.s[s - 7] = v;
@@ -92,9 +130,11 @@ struct PlaneLoader {
 
 struct SoaLoader {
     SoaSrc src;
+    static size_t smem_bytes(const SoaSrc&) { return 0; }
+    __device__ __forceinline__ void stage(unsigned char*) const {}
     __device__ __forceinline__ int64_t count() const { return src.n; }
     template <int DEG, int S0, int S1>
-    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a) const {
+    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a, const unsigned char*) const {
         constexpr int shdim = SplatIn<DEG>::SHD;
         if constexpr (S0 == 0) {
 #pragma unroll
@@ -258,19 +298,21 @@ __global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
                                                       unsigned long long* __restrict__ ctr,
                                                       int32_t* __restrict__ dbg_rect,
                                                       double* __restrict__ dbg_depth) {
+    extern __shared__ __align__(16) unsigned char proj_smem[];
+    ld.stage(proj_smem);
     const int64_t n = ld.count();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = false;
     uint64_t key = ~0ull;
     if (i < n) {
         SplatIn<DEG> a;
-        ld.template load<DEG, 0, 11>((uint32_t)i, a);
+        ld.template load<DEG, 0, 11>((uint32_t)i, a, proj_smem);
         const ProjOut o = project_one(a, cam);
         alive = o.alive;
         if (dbg_depth) dbg_depth[i] = o.depth;
         if (alive) {
             key = (uint64_t)__double_as_longlong(o.depth);
-            ld.template load<DEG, 11, 11 + SplatIn<DEG>::SHD>((uint32_t)i, a);
+            ld.template load<DEG, 11, 11 + SplatIn<DEG>::SHD>((uint32_t)i, a, proj_smem);
             double rgb[3];
             sh_color(a, cam, rgb);
             const double det = o.cov[0] * o.cov[3] - o.cov[1] * o.cov[1];
@@ -325,9 +367,15 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
                     int32_t* dbg_rect, double* dbg_depth, cudaStream_t s) {
     if (n <= 0) return;
     const unsigned blocks = (unsigned)((n + 127) / 128);
-#define GSV_PROJ(D)                                                                              \
-    project_kernel<Loader, D><<<blocks, 128, 0, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, \
-                                                     w->ctr, dbg_rect, dbg_depth)
+    const size_t smem = Loader::smem_bytes(ld.src);
+#define GSV_PROJ(D)                                                                                 \
+    do {                                                                                            \
+        if (smem > 48 * 1024)                                                                       \
+            cudaFuncSetAttribute(project_kernel<Loader, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem);                                                        \
+        project_kernel<Loader, D><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, \
+                                                            w->ctr, dbg_rect, dbg_depth);           \
+    } while (0)
     switch (sh_degree) {
         case 0: GSV_PROJ(0); break;
         case 1: GSV_PROJ(1); break;
