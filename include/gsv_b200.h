@@ -158,6 +158,16 @@ int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos,
                    const double* rot, const double* scl, const double* opac, const double* sh,
                    const gsv_camera* cam, float* out_rgb, uint8_t* out_rgb8,
                    gsv_render_stats* stats);
+/* render(list[Splat2D]) (render.py:359-379) on device fp64 arrays:
+ * means (n,2), cov2d (n,2,2), depth (n), colors (n,3), opacities (n);
+ * rects from cov2d as render() computes them, stable depth order. */
+int gsv_render_splats2d(gsv_session* s, int64_t n, const double* means, const double* cov2d,
+                        const double* depth, const double* colors, const double* opac,
+                        const gsv_camera* cam, float* out_rgb, uint8_t* out_rgb8,
+                        gsv_render_stats* stats);
+/* psnr (metrics.py:31-38) building block: sum over n elements of (a - b)^2
+ * in fp64, a and b device arrays of fp32 (is_f64 = 0) or fp64; *out is host. */
+int gsv_sqdiff(gsv_session* s, const void* a, const void* b, int64_t n, int is_f64, double* out);
 /* reconstruct_frame's fold (motion.py:165-235), in place on device SoA arrays:
  * for each of nd deltas (device pointer tables on the host side):
  *   q <- normalize(dq * q); p += dt; s <- max(s + ds, 1e-7);

@@ -8,14 +8,14 @@ bound through the C ABI in include/gsv_b200.h.
 from .errors import CodecError, FormatError, GsvError, InvalidInputError, StreamError
 from .types import (Camera, ChannelEntry, ChannelId, CodedPayload, ContainerInfo, DecodedGroup,
                     DecodedVideo, FrameDelta, GaussianSet, GroupDirectory, Image, LayeredFrame,
-                    Plane, ResidualDelta, RigidDelta, load_camera, sh_coeff_count)
+                    Plane, ResidualDelta, RigidDelta, Splat2D, load_camera, sh_coeff_count)
 
 __version__ = "0.1.0"
 
 _API = ("DeviceVideo", "Session", "decode_planes", "decode_video", "default_session",
-        "project_debug", "read_container_info", "read_layers", "read_structure",
-        "reconstruct_frame", "reconstruct_frame_tensors", "render_progressive", "render_set",
-        "render_soa_tensors")
+        "load_raw_floats", "project_debug", "psnr", "read_container_info", "read_layers",
+        "read_structure", "reconstruct_frame", "reconstruct_frame_tensors", "render",
+        "render_progressive", "render_set", "render_soa_tensors", "write_ppm", "write_raw_floats")
 
 
 def __getattr__(name):  # lazy: importing torch is only needed for the GPU API
@@ -31,4 +31,4 @@ def __getattr__(name):  # lazy: importing torch is only needed for the GPU API
 __all__ = ["CodecError", "FormatError", "GsvError", "InvalidInputError", "StreamError", "Camera",
            "ChannelEntry", "ChannelId", "CodedPayload", "ContainerInfo", "DecodedGroup",
            "DecodedVideo", "FrameDelta", "GaussianSet", "GroupDirectory", "Image", "LayeredFrame",
-           "Plane", "ResidualDelta", "RigidDelta", "load_camera", "sh_coeff_count", *_API]
+           "Plane", "ResidualDelta", "RigidDelta", "Splat2D", "load_camera", "sh_coeff_count", *_API]

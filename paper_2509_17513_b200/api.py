@@ -17,6 +17,9 @@ prefix resident in HBM that renders frames into device tensors.
 from __future__ import annotations
 
 import ctypes
+import math
+import os
+import tempfile
 import io
 import threading
 from pathlib import Path
@@ -447,6 +450,94 @@ def render_soa_tensors(tensors, sh_degree: int, cam, session: Session | None = N
         return out, {"n_splats": st.n_splats, "n_visible": st.n_visible, "n_keys": st.n_keys,
                      "n_keys_emitted": st.n_keys_emitted, "tiles": (st.tiles_x, st.tiles_y)}
     return out
+
+
+def render(splats, cam) -> Image:
+    """render (render.py:359-379): composite projected splats on the GPU;
+    depth order is stable (ties keep input order); no splats -> background."""
+    if not splats:
+        bg = np.asarray(cam.background, dtype=np.float64)
+        return Image(pixels=np.tile(bg, (cam.height, cam.width, 1)))
+    s = default_session()
+    dev = torch.device("cuda", s.device)
+    cols = [np.stack([np.asarray(sp.mean2d, np.float64) for sp in splats]),
+            np.stack([np.asarray(sp.cov2d, np.float64).reshape(4) for sp in splats]),
+            np.array([float(sp.depth) for sp in splats]),
+            np.stack([np.asarray(sp.color, np.float64) for sp in splats]),
+            np.array([float(sp.base_opacity) for sp in splats])]
+    t = [torch.from_numpy(np.ascontiguousarray(c)).to(dev) for c in cols]
+    c = camera_struct(cam)
+    out = torch.empty((c.height, c.width, 3), dtype=torch.float32, device=dev)
+    _pre(s)
+    check(s.lib.gsv_render_splats2d(s.handle, len(splats), *(_ptr(x) for x in t), ctypes.byref(c),
+                                    _ptr(out), None, None))
+    _post(s)
+    return Image(pixels=out.cpu().numpy().astype(np.float64))
+
+
+PSNR_CAP = 99.0  # metrics.py:24
+
+
+def psnr(gt, pred) -> float:
+    """psnr (metrics.py:31-38): 10*log10(1/MSE) over all channels, capped at
+    99 dB.  Images or device/host tensors; the squared-difference sum runs on
+    the GPU in fp64."""
+    a = gt.pixels if isinstance(gt, Image) else gt
+    b = pred.pixels if isinstance(pred, Image) else pred
+    if tuple(a.shape) != tuple(b.shape):
+        raise InvalidInputError("image dimensions differ")
+    s = default_session()
+    dev = torch.device("cuda", s.device)
+
+    def dev_t(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        return t.to(dev).contiguous()
+    ta, tb = dev_t(a), dev_t(b)
+    if ta.dtype != tb.dtype or ta.dtype not in (torch.float32, torch.float64):
+        ta, tb = ta.to(torch.float64), tb.to(torch.float64)
+    out = ctypes.c_double(0.0)
+    _pre(s)
+    check(s.lib.gsv_sqdiff(s.handle, _ptr(ta), _ptr(tb), ta.numel(), 1 if ta.dtype == torch.float64 else 0,
+                           ctypes.byref(out)))
+    _post(s)
+    n = ta.numel()
+    mse = out.value / n if n else 0.0
+    if mse == 0.0:
+        return PSNR_CAP
+    return min(10.0 * math.log10(1.0 / mse), PSNR_CAP)
+
+
+def _atomic_write(path, blob: bytes) -> None:
+    """splatio._atomic_write (splatio.py:107-117)."""
+    path = Path(path)
+    fd, tmp = tempfile.mkstemp(dir=path.parent or ".", prefix=path.name + ".")
+    try:
+        with os.fdopen(fd, "wb") as f:
+            f.write(blob)
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def write_ppm(img: Image, path) -> None:
+    """write_ppm (render.py:165-169): 8-bit binary PPM (P6)."""
+    u8 = np.clip(np.floor(img.pixels * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    header = f"P6\n{img.width} {img.height}\n255\n".encode()
+    _atomic_write(path, header + u8.tobytes())
+
+
+def write_raw_floats(img: Image, path) -> None:
+    """write_raw_floats (render.py:172-178): lossless .npy dump."""
+    import io
+    buf = io.BytesIO()
+    np.save(buf, img.pixels)
+    _atomic_write(path, buf.getvalue())
+
+
+def load_raw_floats(path) -> Image:
+    return Image(pixels=np.load(path))
 
 
 def render_set(gset, cam) -> Image:

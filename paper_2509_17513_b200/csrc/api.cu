@@ -737,6 +737,29 @@ int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos, 
     return render_soa(src, make_cam(*cam), &s->work, out_rgb, out_rgb8, stats, s->stream);
 }
 
+int gsv_render_splats2d(gsv_session* s, int64_t n, const double* means, const double* cov2d,
+                        const double* depth, const double* colors, const double* opac,
+                        const gsv_camera* cam, float* out_rgb, uint8_t* out_rgb8, gsv_render_stats* stats) {
+    if (n < 0) return fail(GSV_E_INVALID_INPUT, "negative splat count");
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    Splat2DSrc src{means, cov2d, depth, colors, opac, n};
+    return render_splats2d(src, make_cam(*cam), &s->work, out_rgb, out_rgb8, stats, s->stream);
+}
+
+int gsv_sqdiff(gsv_session* s, const void* a, const void* b, int64_t n, int is_f64, double* out) {
+    double* d = nullptr;
+    GSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(double), s->stream));
+    if (is_f64)
+        launch_sqdiff_f64(static_cast<const double*>(a), static_cast<const double*>(b), n, d, s->stream);
+    else
+        launch_sqdiff_f32(static_cast<const float*>(a), static_cast<const float*>(b), n, d, s->stream);
+    count_launch(1);
+    GSV_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    GSV_CUDA(cudaFreeAsync(d, s->stream));
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    return GSV_OK;
+}
+
 int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* pos, const double* rot,
                       const double* scl, const double* opac, const double* sh, const gsv_camera* cam,
                       int32_t* rects, double* depth, int32_t* order, int32_t* tile_count,

@@ -124,6 +124,16 @@ struct SoaSrc {
     int64_t n;
 };
 
+// projected splats (render(list[Splat2D]) inputs), device fp64
+struct Splat2DSrc {
+    const double* means;   // (n,2)
+    const double* cov;     // (n,2,2)
+    const double* depth;   // (n)
+    const double* colors;  // (n,3)
+    const double* opac;    // (n)
+    int64_t n;
+};
+
 // Camera as the kernels see it (render.py:43-120)
 struct CamDev {
     double R[9];
@@ -223,6 +233,11 @@ int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* 
                   uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
 int render_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
                uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
+int render_splats2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+                    uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
+// sum of squared differences of two device arrays (fp32 or fp64), into *out (device)
+void launch_sqdiff_f32(const float* a, const float* b, int64_t n, double* out, cudaStream_t s);
+void launch_sqdiff_f64(const double* a, const double* b, int64_t n, double* out, cudaStream_t s);
 int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s);

@@ -397,6 +397,88 @@ void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int
 }
 
 // ---------------------------------------------------------------------------
+// render(list[Splat2D]) (render.py:359-379): projected splats in, rects
+// recomputed from cov2d exactly as render() does, then the common record /
+// depth-key layout.  Depth keys are the order-preserving u64 image of the
+// fp64 depth (any sign), so the stable radix sort reproduces
+// argsort(depth, kind="stable") (render.py:343).  Splats with an empty rect
+// draw nothing in the reference and are dropped here.
+// -0.0 sorts as +0.0 and every NaN after +inf, like numpy's argsort.
+__device__ __forceinline__ uint64_t orderable_key(double d) {
+    if (d == 0.0) d = 0.0;
+    if (d != d) return ~0ull - 1;
+    const uint64_t b = (uint64_t)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+__global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* __restrict__ means,
+                                                      const double* __restrict__ cov,
+                                                      const double* __restrict__ depth,
+                                                      const double* __restrict__ colors,
+                                                      const double* __restrict__ opac, CamDev cam,
+                                                      uint64_t* __restrict__ dkey, uint32_t* __restrict__ didx,
+                                                      SplatRec* __restrict__ rec,
+                                                      unsigned long long* __restrict__ ctr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool alive = false;
+    uint64_t key = ~0ull;
+    if (i < n) {
+        const double mx = means[2 * i], my = means[2 * i + 1];
+        const double A = cov[4 * i], B = cov[4 * i + 1], C = cov[4 * i + 3];
+        const double hm = (A - C) / 2;
+        const double lam = (A + C) / 2 + sqrt(hm * hm + B * B);
+        const double radius = ceil(3.0 * sqrt(np_max(lam, 0.0)));
+        const double x0 = np_max(floor(mx - radius), 0.0), x1 = np_min(floor(mx + radius) + 1, (double)cam.width);
+        const double y0 = np_max(floor(my - radius), 0.0), y1 = np_min(floor(my + radius) + 1, (double)cam.height);
+        alive = x0 < x1 && y0 < y1;
+        if (alive) {
+            key = orderable_key(depth[i]);
+            const double det = A * C - cov[4 * i + 1] * cov[4 * i + 1];
+            const double l2e = 1.4426950408889634;
+            SplatRec r;
+            r.fx0 = (float)x0;
+            r.fy0 = (float)y0;
+            r.fx1 = (float)x1;
+            r.fy1 = (float)y1;
+            r.ox = (float)(mx - x0);
+            r.oy = (float)(my - y0);
+            r.ca = (float)(-0.5 * l2e * (C / det));
+            r.cb = (float)(-l2e * (-B / det));
+            r.cc = (float)(-0.5 * l2e * (A / det));
+            r.r = (float)colors[3 * i];
+            r.g = (float)colors[3 * i + 1];
+            r.b = (float)colors[3 * i + 2];
+            r.op = (float)opac[i];
+            r.rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
+            r.ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
+            r.pad = 0;
+            rec[i] = r;
+        }
+        dkey[i] = key;
+        didx[i] = (uint32_t)i;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, alive);
+    uint64_t kmin = alive ? key : ~0ull, kmax = alive ? key : 0ull;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        kmin = min(kmin, (uint64_t)__shfl_xor_sync(0xffffffffu, kmin, off));
+        kmax = max(kmax, (uint64_t)__shfl_xor_sync(0xffffffffu, kmax, off));
+    }
+    if ((threadIdx.x & 31) == 0 && m) {
+        atomicAdd(ctr + 0, (unsigned long long)__popc(m));
+        atomicMin(ctr + 2, (unsigned long long)kmin);
+        atomicMax(ctr + 3, (unsigned long long)kmax);
+    }
+}
+
+void launch_splat2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s) {
+    if (src.n <= 0) return;
+    splat2d_kernel<<<(unsigned)((src.n + 127) / 128), 128, 0, s>>>(src.n, src.means, src.cov, src.depth,
+                                                                   src.colors, src.opac, cam, w->dkey[0],
+                                                                   w->didx[0], w->rec, w->ctr);
+}
+
+// ---------------------------------------------------------------------------
 // reconstruct_frame fold: apply_rigid then apply_residual (motion.py:165-193)
 // ---------------------------------------------------------------------------
 __global__ void fold_kernel(int64_t n, int shdim, double* __restrict__ pos, double* __restrict__ rot,

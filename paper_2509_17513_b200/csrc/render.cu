@@ -23,6 +23,7 @@
 namespace gsv {
 
 void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
+void launch_splat2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
 void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* dbg_rect,
                         double* dbg_depth, cudaStream_t s);
 
@@ -553,6 +554,47 @@ int render_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, float* out_r
                uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s) {
     auto proj = [&]() { launch_project_soa(src, cam, w, nullptr, nullptr, s); };
     return render_checked(src.n, cam, w, proj, out_rgb, out_rgb8, stats, s);
+}
+
+int render_splats2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
+                    uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s) {
+    auto proj = [&]() { launch_splat2d(src, cam, w, s); };
+    return render_checked(src.n, cam, w, proj, out_rgb, out_rgb8, stats, s);
+}
+
+// ---------------------------------------------------------------------------
+// psnr (metrics.py:31-38): the sum of squared differences on the device
+// (fp64 accumulation); the host takes mean, log10 and the 99 dB cap.
+template <typename T>
+__global__ void sqdiff_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t n,
+                              double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = (double)a[i] - (double)b[i];
+        acc = fma(d, d, acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) t += ws[k];
+        atomicAdd(out, t);
+    }
+}
+
+void launch_sqdiff_f32(const float* a, const float* b, int64_t n, double* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(double), s);
+    const int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (n > 0) sqdiff_kernel<float><<<(unsigned)std::max<int64_t>(g, 1), 256, 0, s>>>(a, b, n, out);
+}
+
+void launch_sqdiff_f64(const double* a, const double* b, int64_t n, double* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(double), s);
+    const int64_t g = std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (n > 0) sqdiff_kernel<double><<<(unsigned)std::max<int64_t>(g, 1), 256, 0, s>>>(a, b, n, out);
 }
 
 __global__ void copy_order(const uint32_t* __restrict__ idx0, const uint32_t* __restrict__ idx1,

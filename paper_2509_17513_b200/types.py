@@ -242,6 +242,17 @@ def load_camera(path) -> Camera:
 
 
 @dataclass(frozen=True)
+class Splat2D:
+    """A projected Gaussian ready for compositing (render.py:132-140)."""
+
+    mean2d: np.ndarray    # (2,) pixel coordinates
+    cov2d: np.ndarray     # (2, 2) symmetric positive definite, px^2
+    depth: float          # camera-space z
+    color: np.ndarray     # (3,) RGB in [0, 1]
+    base_opacity: float
+
+
+@dataclass(frozen=True)
 class Image:
     """An HxWx3 float image with channels in [0, 1]."""
 

@@ -296,7 +296,44 @@ def make_known_answer(doc):
     doc["known_answer"] = {"camera": cam_json(cam), "accept": scenes}
 
 
+def make_render2d(doc):
+    """render(list[Splat2D]) on random projected splats (ragged rects at the
+    image border, exact depth ties, negative depths, empty rects) and psnr
+    values between reference images (metrics.py:31-38)."""
+    from gsv.metrics import psnr
+    from gsv.render import Splat2D, render
+    rng = np.random.default_rng(4242)
+    cam = Camera(rotation=np.eye(3), translation=np.zeros(3), fx=90.0, fy=90.0,
+                 cx=40.0, cy=30.0, width=80, height=60, near=0.1, background=(0.1, 0.2, 0.3))
+    n = 400
+    means = rng.uniform(-10, 90, size=(n, 2))
+    sx = rng.uniform(0.3, 6.0, n)
+    sy = rng.uniform(0.3, 6.0, n)
+    rho = rng.uniform(-0.8, 0.8, n)
+    cov = np.stack([np.stack([sx * sx, rho * sx * sy], -1), np.stack([rho * sx * sy, sy * sy], -1)], -2)
+    depth = np.round(rng.uniform(-1.0, 3.0, n), 1)  # many exact ties, some negative
+    colors = rng.uniform(0, 1, size=(n, 3))
+    opac = rng.uniform(0.05, 1.0, n)
+    opac[::37] = 0.0
+    splats = [Splat2D(mean2d=means[i], cov2d=cov[i], depth=float(depth[i]), color=colors[i],
+                      base_opacity=float(opac[i])) for i in range(n)]
+    img = render(splats, cam).pixels
+    img_half = render(splats[: n // 2], cam).pixels
+    arrays = {"means": means, "cov": cov, "depth": depth, "colors": colors, "opac": opac,
+              "img": img, "img_half": img_half}
+    np.savez_compressed(OUT / "renders" / "render2d.npz", **arrays)
+    from gsv.render import Image as RImage
+    doc["render2d"] = {"camera": cam_json(cam), "n": n,
+                       "psnr_full_half": psnr(RImage(img), RImage(img_half)),
+                       "psnr_same": psnr(RImage(img), RImage(img))}
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--only-render2d":
+        doc = json.loads((OUT / "golden.json").read_text())
+        make_render2d(doc)
+        (OUT / "golden.json").write_text(json.dumps(doc, indent=1, default=float) + "\n")
+        return
     if TMP.exists():
         shutil.rmtree(TMP)
     TMP.mkdir(parents=True)
@@ -317,6 +354,7 @@ def main():
     make_errors(doc)
     make_progressive(doc)
     make_known_answer(doc)
+    make_render2d(doc)
     (OUT / "golden.json").write_text(json.dumps(doc, indent=1, default=float) + "\n")
     print("wrote", OUT)
 

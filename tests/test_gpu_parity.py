@@ -217,3 +217,27 @@ def test_config2_frame_parity(gsvb):
                 assert st["n_visible"] == idx.size
                 assert st["n_keys"] == int(O.tile_counts(rects).sum())
                 assert np.max(np.abs(img - ref)) <= MAX_ABS, (k, t)
+
+
+@pytest.mark.gpu
+def test_render2d_and_psnr_gpu(gsvb):
+    """render(list[Splat2D]) on the GPU vs the reference image (stable depth
+    order with exact ties and negative depths, border-clipped and empty
+    rects, zero opacities): max-abs <= 2e-3; psnr on the GPU vs the
+    reference's value |dPSNR| <= 0.01 dB."""
+    from golden_util import Cam, doc, renders
+    d = doc()["render2d"]
+    r = renders("render2d")
+    cam = Cam.from_json(d["camera"])
+    splats = [gsvb.Splat2D(mean2d=r["means"][i], cov2d=r["cov"][i], depth=float(r["depth"][i]),
+                           color=r["colors"][i], base_opacity=float(r["opac"][i]))
+              for i in range(len(r["depth"]))]
+    img = gsvb.render(splats, cam).pixels
+    assert np.max(np.abs(img - r["img"])) <= 2e-3
+    half = gsvb.render(splats[: len(splats) // 2], cam).pixels
+    assert np.max(np.abs(half - r["img_half"])) <= 2e-3
+    assert abs(gsvb.psnr(img, half) - d["psnr_full_half"]) <= 0.01
+    assert abs(gsvb.psnr(gsvb.Image(r["img"]), gsvb.Image(r["img_half"])) - d["psnr_full_half"]) <= 1e-9
+    assert gsvb.psnr(img, img) == 99.0
+    bg = gsvb.render([], cam).pixels
+    assert np.array_equal(bg, np.tile(np.asarray(cam.background), (cam.height, cam.width, 1)))

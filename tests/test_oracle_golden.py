@@ -136,3 +136,18 @@ def test_tile_keys_consistent_with_counts():
     assert np.all(np.diff(tiles) >= 0)
     for t in np.unique(tiles)[:20]:
         assert np.all(np.diff(ranks[tiles == t]) > 0)
+
+
+def test_render2d_and_psnr_oracle():
+    """render(list[Splat2D]) (render.py:359-379) and psnr (metrics.py:31-38)
+    restated in the oracle, pinned to the reference's outputs."""
+    from golden_util import Cam, doc, renders
+    d = doc()["render2d"]
+    r = renders("render2d")
+    cam = Cam.from_json(d["camera"])
+    img = O.render2d(r["means"], r["cov"], r["depth"], r["colors"], r["opac"], cam)
+    assert np.max(np.abs(img - r["img"])) <= 1e-12
+    assert O.psnr(r["img"], r["img_half"]) == d["psnr_full_half"]
+    assert O.psnr(r["img"], r["img"]) == d["psnr_same"] == 99.0
+    empty = O.render2d(np.zeros((0, 2)), np.zeros((0, 2, 2)), [], np.zeros((0, 3)), [], cam)
+    assert np.array_equal(empty, np.tile(np.asarray(cam.background), (cam.height, cam.width, 1)))
