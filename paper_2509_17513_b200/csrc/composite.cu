@@ -55,6 +55,57 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
     return v;
 }
 
+// Packed fp32 pair arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): the
+// compositor's per-pixel fp32 work runs on row pairs, halving its FMA-pipe
+// issue.  Rounding is the scalar ops' (.rn), so results are bit-identical to
+// evaluating the pair one row at a time.
+struct f2 {
+    float x, y;
+};
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// Upper bound of the power of one pixel: 0 when the pixel composites this
+// splat (bit `bit` of m set: inside the rect; and T >= 1e-4, render.py:
+// 316-318), -inf otherwise (alpha 0: C and T unchanged).
+__device__ __forceinline__ float pix_lim(uint32_t m, uint32_t bit, float T) {
+    float r;
+    asm("{\n\t.reg .pred pm, pt;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 pm, t, 0;\n\t"
+        "setp.ge.and.f32 pt, %3, 0f38D1B717, pm;\n\t"
+        "selp.f32 %0, 0f00000000, 0fFF800000, pt;\n\t}"
+        : "=f"(r) : "r"(m), "r"(bit), "f"(T));
+    return r;
+}
+__device__ __forceinline__ float ex2f(float x) {
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
+    return e;
+}
+
 // Warp-per-strip compositor.  A 16x16 tile is split into 16/(2*ROWS) strips
 // of 16 x 2*ROWS pixels, one warp each; lane l owns column l & 15 and ROWS
 // consecutive rows of the strip's upper (l < 16) or lower half.  The warp
@@ -66,7 +117,7 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
 // pixel), power clamp, 0.99 alpha cap, alpha <= 0 skip, fp32, fixed order.
 // The quadratic form is evaluated as A + dy (B + C dy) with A, B per
 // (record, column) -- a different fp32 rounding of the same fp64 quantity.
-template <int ROWS>
+template <int ROWS, bool PACKED>
 __global__ void __launch_bounds__(128) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
@@ -143,27 +194,56 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             const float dx = (pxf - rc.x) - a.x;
             const float A = a.z * dx * dx, B = a.w * dx;
             const float dy0 = (py0f - rc.y) - a.y;
-            // branch-free over the lane's rows: a pixel outside the rect or
-            // already at T < 1e-4 gets alpha 0, and alpha <= 0 composites as a
-            // no-op (C, T unchanged), so the ROWS chains interleave
+            if constexpr (PACKED) {
+                // row pairs; a pixel outside the rect or at T < 1e-4 gets power
+                // -inf (alpha 0: C, T unchanged); opacities are >= 0 (clamped
+                // in the record: a negative one draws nothing in the reference)
+                const f2 A2{A, A}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
+                const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};
 #pragma unroll
-            for (int j = 0; j < ROWS; j++) {
-                const float dy = dy0 + (float)j;
-                const float pw = fminf(fmaf(fmaf(b.x, dy, B), dy, A), 0.0f);
-                float e;
-                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(pw));
-                const float al = fminf(fmaxf(op * e, 0.0f), 0.99f);
-                float alpha;  // row bit of m and T >= 1e-4, as one bit test + one compare
-                asm("{\n\t.reg .pred pm, pt;\n\t.reg .b32 t;\n\t"
-                    "and.b32 t, %1, %2;\n\tsetp.ne.b32 pm, t, 0;\n\t"
-                    "setp.ge.and.f32 pt, %3, 0f38D1B717, pm;\n\t"
-                    "selp.f32 %0, %4, 0f00000000, pt;\n\t}"
-                    : "=f"(alpha) : "r"(m), "r"(1u << j), "f"(T[j]), "f"(al));
-                const float w = T[j] * alpha;
-                c0[j] = fmaf(w, b.y, c0[j]);
-                c1[j] = fmaf(w, b.z, c1[j]);
-                c2[j] = fmaf(w, b.w, c2[j]);
-                T[j] = T[j] - w;  // T (1 - alpha)
+                for (int j = 0; j < ROWS; j += 2) {
+                    const f2 dy = add2(D2, f2{(float)j, (float)(j + 1)});
+                    f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
+                    pw.x = fminf(pw.x, pix_lim(m, 1u << j, T[j]));
+                    pw.y = fminf(pw.y, pix_lim(m, 1u << (j + 1), T[j + 1]));
+                    f2 al = mul2(O2, f2{ex2f(pw.x), ex2f(pw.y)});
+                    al.x = fminf(al.x, 0.99f);
+                    al.y = fminf(al.y, 0.99f);
+                    const f2 w = mul2(f2{T[j], T[j + 1]}, al);
+                    f2 c = fma2(w, R2, f2{c0[j], c0[j + 1]});
+                    c0[j] = c.x;
+                    c0[j + 1] = c.y;
+                    c = fma2(w, G2, f2{c1[j], c1[j + 1]});
+                    c1[j] = c.x;
+                    c1[j + 1] = c.y;
+                    c = fma2(w, Bl2, f2{c2[j], c2[j + 1]});
+                    c2[j] = c.x;
+                    c2[j + 1] = c.y;
+                    const f2 t = fma2(w, M1, f2{T[j], T[j + 1]});  // T (1 - alpha)
+                    T[j] = t.x;
+                    T[j + 1] = t.y;
+                }
+            } else {
+                // branch-free over the lane's rows: a pixel outside the rect or
+                // already at T < 1e-4 gets alpha 0, and alpha <= 0 composites as a
+                // no-op (C, T unchanged), so the ROWS chains interleave
+#pragma unroll
+                for (int j = 0; j < ROWS; j++) {
+                    const float dy = dy0 + (float)j;
+                    const float pw = fminf(fmaf(fmaf(b.x, dy, B), dy, A), 0.0f);
+                    const float al = fminf(fmaxf(op * ex2f(pw), 0.0f), 0.99f);
+                    float alpha;  // row bit of m and T >= 1e-4, as one bit test + one compare
+                    asm("{\n\t.reg .pred pm, pt;\n\t.reg .b32 t;\n\t"
+                        "and.b32 t, %1, %2;\n\tsetp.ne.b32 pm, t, 0;\n\t"
+                        "setp.ge.and.f32 pt, %3, 0f38D1B717, pm;\n\t"
+                        "selp.f32 %0, %4, 0f00000000, pt;\n\t}"
+                        : "=f"(alpha) : "r"(m), "r"(1u << j), "f"(T[j]), "f"(al));
+                    const float w = T[j] * alpha;
+                    c0[j] = fmaf(w, b.y, c0[j]);
+                    c1[j] = fmaf(w, b.z, c1[j]);
+                    c2[j] = fmaf(w, b.w, c2[j]);
+                    T[j] = T[j] - w;  // T (1 - alpha)
+                }
             }
         }
         // live pixels for the early exit and the skip test, once per batch
@@ -221,13 +301,24 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
     const unsigned grid = (unsigned)((warps + 3) / 4);
-#define GSV_COMPOSITE(R)                                                                             \
-    composite_strip_kernel<R><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
-                                                   cam.height, ntx, ntiles, first, last, cam.bg[0],   \
-                                                   cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
-    if (rows == 8) GSV_COMPOSITE(8);
-    else if (rows == 4) GSV_COMPOSITE(4);
-    else GSV_COMPOSITE(2);
+    static int packed = -1;
+    if (packed < 0) {
+        const char* e = getenv("GSV_COMPOSITE_PACKED");
+        packed = e ? atoi(e) : 1;
+    }
+#define GSV_COMPOSITE(R, P)                                                                             \
+    composite_strip_kernel<R, P><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
+                                                      cam.height, ntx, ntiles, first, last, cam.bg[0],   \
+                                                      cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
+    if (packed) {
+        if (rows == 8) GSV_COMPOSITE(8, true);
+        else if (rows == 4) GSV_COMPOSITE(4, true);
+        else GSV_COMPOSITE(2, true);
+    } else {
+        if (rows == 8) GSV_COMPOSITE(8, false);
+        else if (rows == 4) GSV_COMPOSITE(4, false);
+        else GSV_COMPOSITE(2, false);
+    }
 #undef GSV_COMPOSITE
 }
 

@@ -458,6 +458,26 @@ static void round_bounds(int64_t n, std::vector<uint32_t>* b) {
     b->push_back((uint32_t)std::max<int64_t>(n, 0));
 }
 
+// Dev diagnostics: GSV_DEBUG_SKIP lists stages whose kernels are not
+// launched (composite, tsort, dsort, emit) -- wrong images, used only to
+// measure what each stage costs in the frame-parallel steady state.
+static unsigned debug_skip() {
+    static int init = 0;
+    static unsigned mask = 0;
+    if (!init) {
+        const char* e = getenv("GSV_DEBUG_SKIP");
+        if (e) {
+            if (strstr(e, "composite")) mask |= 1;
+            if (strstr(e, "tsort")) mask |= 2;
+            if (strstr(e, "dsort")) mask |= 4;
+            if (strstr(e, "emit")) mask |= 8;
+            if (strstr(e, "project")) mask |= 16;
+        }
+        init = 1;
+    }
+    return mask;
+}
+
 // Enqueue one frame.  `project` enqueues the projection kernel into w.
 template <class Proj>
 static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj project,
@@ -474,12 +494,13 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     prof_mark(ST_PROJECT, s);
     reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, reinterpret_cast<uint32_t*>(w->tile_done),
                                           ntiles, open_word(composite_rows()));
-    project();
+    const unsigned skip = debug_skip();
+    if (!(skip & 16)) project();
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
         depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
-        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
+        if (!(skip & 4)) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         count_launch(2 + radix_launches(4, true));
     }
@@ -495,17 +516,18 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         prof_mark(ST_EMIT, s);
         const unsigned ge = std::max(1u, (unsigned)((b - a + kEmitTile - 1) / kEmitTile));
         uint32_t* th = sc.ghist + 1024 * (1 + (int)std::min<size_t>(j, kHistRegions - 2));
-        round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b,
+        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b,
                                                       reinterpret_cast<const uint32_t*>(w->tile_done), w->tkey[0],
                                                       w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
                                                       w->ticket, ++w->epoch, th, tp);
         count_launch(1);
         prof_mark(ST_TSORT, s);
-        radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
+        if (!(skip & 2)) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
         count_launch(radix_launches(tp, true));
         prof_mark(ST_COMPOSITE, s);
-        launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
-                               w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
+        if (!(skip & 1))
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+                                   w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
         count_launch(1);
     }
     prof_mark(ST_COUNT, s);
