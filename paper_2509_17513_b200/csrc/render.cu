@@ -452,9 +452,26 @@ static int tile_passes(int ntiles) {
 // DESIGN.md).
 static void round_bounds(int64_t n, std::vector<uint32_t>* b) {
     b->clear();
-    const int64_t r1 = std::max<int64_t>(32768, n / 10);
     b->push_back(0);
-    if (n > r1) b->push_back((uint32_t)r1);
+    static std::vector<int64_t> fixed;  // dev tuning: GSV_ROUNDS="r1,r2,..." (absolute ranks)
+    static int init = 0;
+    if (!init) {
+        if (const char* e = getenv("GSV_ROUNDS")) {
+            for (const char* q = e; *q;) {
+                fixed.push_back(atoll(q));
+                while (*q && *q != ',') q++;
+                if (*q == ',') q++;
+            }
+        }
+        init = 1;
+    }
+    if (!fixed.empty()) {
+        for (int64_t r : fixed)
+            if (r > (int64_t)b->back() && r < n) b->push_back((uint32_t)r);
+    } else {
+        const int64_t r1 = std::max<int64_t>(32768, n / 10);
+        if (n > r1) b->push_back((uint32_t)r1);
+    }
     b->push_back((uint32_t)std::max<int64_t>(n, 0));
 }
 

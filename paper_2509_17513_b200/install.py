@@ -10,15 +10,17 @@ from __future__ import annotations
 
 
 def install(verbose: bool = False) -> dict:
+    import importlib
+
     import gsv  # noqa: F401  (the reference must be importable)
-    import gsv.cli as gcli
-    import gsv.codec as gcodec
-    import gsv.container as gcont
-    import gsv.gaussians as ggauss
-    import gsv.motion as gmotion
-    import gsv.pipeline as gpipe
-    import gsv.quantize as gquant
-    import gsv.render as grender
+
+    # by module path: `gsv.render` as an attribute is the render() function
+    # the package re-exports, not the submodule
+    def mod(name):
+        return importlib.import_module("gsv." + name)
+    gcli, gcodec, gcont = mod("cli"), mod("codec"), mod("container")
+    ggauss, gmetrics, gmotion = mod("gaussians"), mod("metrics"), mod("motion")
+    gpipe, gquant, grender = mod("pipeline"), mod("quantize"), mod("render")
 
     from . import api
 
@@ -54,6 +56,12 @@ def install(verbose: bool = False) -> dict:
     def reconstruct_frame(group_keyframe, deltas, t, up_to_layer=None):
         return _set(api.reconstruct_frame(group_keyframe, deltas, t, up_to_layer))
 
+    def render(splats, cam):
+        return grender.Image(pixels=api.render(splats, cam).pixels)
+
+    def psnr(gt, pred):
+        return api.psnr(gt.pixels, pred.pixels)
+
     patches = {
         (gpipe, "decode_video"): decode_video, (gcli, "decode_video"): decode_video,
         (gcont, "read_layers"): read_layers, (gpipe, "read_layers"): read_layers,
@@ -62,6 +70,8 @@ def install(verbose: bool = False) -> dict:
         (grender, "render_progressive"): render_progressive,
         (gmotion, "reconstruct_frame"): reconstruct_frame,
         (grender, "reconstruct_frame"): reconstruct_frame,
+        (grender, "render"): render,
+        (gmetrics, "psnr"): psnr, (gcli, "psnr"): psnr,
     }
     old = {}
     for (mod, name), fn in patches.items():
@@ -69,7 +79,7 @@ def install(verbose: bool = False) -> dict:
             old[(mod.__name__, name)] = getattr(mod, name)
             setattr(mod, name, fn)
     for name in ("decode_video", "read_layers", "decode_planes", "render_set",
-                 "render_progressive", "reconstruct_frame"):
+                 "render_progressive", "reconstruct_frame", "render", "psnr"):
         if hasattr(gsv, name):
             setattr(gsv, name, locals()[name])
     if verbose:

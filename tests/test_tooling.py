@@ -97,3 +97,37 @@ def test_streaming_generator_matches_list():
     for x, y in zip(a, b):
         assert np.array_equal(x.positions, y.positions)
         assert np.array_equal(x.sh, y.sh)
+
+
+def test_install_rebinds_reference_entry_points():
+    """install() rebinds the reference's decode/render entry points (and the
+    names gsv.cli bound at import) to this package; checked against a copy
+    of the reference when one is importable (dev container only)."""
+    import importlib
+    import os
+    import sys
+    ref = os.environ.get("GSV_REFERENCE", "/root/reference/pkg")
+    if not os.path.isdir(os.path.join(ref, "src", "gsv")):
+        pytest.skip("reference package not present")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, os.path.join(ref, "src"))
+    try:
+        gsv = importlib.import_module("gsv")
+        gcli = importlib.import_module("gsv.cli")
+        gmetrics = importlib.import_module("gsv.metrics")
+        grender = importlib.import_module("gsv.render")
+        from paper_2509_17513_b200.install import install
+        before = {n: getattr(gsv, n) for n in ("decode_video", "render_set", "render", "psnr")}
+        old = install()
+        try:
+            for n, f in before.items():
+                assert getattr(gsv, n) is not f and getattr(gsv, n).__module__.startswith("paper_2509")
+            assert gcli.render_set is grender.render_set and gcli.psnr is gmetrics.psnr
+            assert ("gsv.render", "render") in old and ("gsv.metrics", "psnr") in old
+        finally:
+            for (mod, name), fn in old.items():
+                setattr(sys.modules[mod], name, fn)
+            for n, f in before.items():
+                setattr(gsv, n, f)
+    finally:
+        sys.path.remove(os.path.join(ref, "src"))
