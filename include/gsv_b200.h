@@ -168,6 +168,10 @@ int gsv_render_splats2d(gsv_session* s, int64_t n, const double* means, const do
 /* psnr (metrics.py:31-38) building block: sum over n elements of (a - b)^2
  * in fp64, a and b device arrays of fp32 (is_f64 = 0) or fp64; *out is host. */
 int gsv_sqdiff(gsv_session* s, const void* a, const void* b, int64_t n, int is_f64, double* out);
+/* ssim (metrics.py:48-65): mean SSIM of the channel-mean images of two
+ * device (height, width, 3) images, fp32 (is_f64 = 0) or fp64; *out is host. */
+int gsv_ssim(gsv_session* s, const void* a, const void* b, int height, int width, int is_f64,
+             double* out);
 /* reconstruct_frame's fold (motion.py:165-235), in place on device SoA arrays:
  * for each of nd deltas (device pointer tables on the host side):
  *   q <- normalize(dq * q); p += dt; s <- max(s + ds, 1e-7);

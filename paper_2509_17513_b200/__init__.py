@@ -12,10 +12,11 @@ from .types import (Camera, ChannelEntry, ChannelId, CodedPayload, ContainerInfo
 
 __version__ = "0.1.0"
 
-_API = ("DeviceVideo", "Session", "decode_planes", "decode_video", "default_session",
-        "load_raw_floats", "project_debug", "psnr", "read_container_info", "read_layers",
+_API = ("DeviceVideo", "Session", "analyze_rd", "d_ssim", "decode_planes", "decode_video",
+        "default_session", "load_raw_floats", "project_debug", "psnr", "read_container_info", "read_layers",
         "read_structure", "reconstruct_frame", "reconstruct_frame_tensors", "render",
-        "render_progressive", "render_set", "render_soa_tensors", "write_ppm", "write_raw_floats")
+        "render_progressive", "render_set", "render_soa_tensors", "ssim", "write_ppm",
+        "write_raw_floats")
 
 
 def __getattr__(name):  # lazy: importing torch is only needed for the GPU API

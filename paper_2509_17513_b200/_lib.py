@@ -89,6 +89,7 @@ _SIGS = {
                             _P]),
     "gsv_render_splats2d": (_I, [_P, _I64, _P, _P, _P, _P, _P, ctypes.POINTER(Camera_t), _P, _P, _P]),
     "gsv_sqdiff": (_I, [_P, _P, _P, _I64, _I, ctypes.POINTER(ctypes.c_double)]),
+    "gsv_ssim": (_I, [_P, _P, _P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
     "gsv_fold_deltas": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
     "gsv_project_debug": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P, ctypes.POINTER(Camera_t), _P, _P,
                                _P, _P, ctypes.POINTER(_I64)]),

@@ -507,6 +507,72 @@ def psnr(gt, pred) -> float:
     return min(10.0 * math.log10(1.0 / mse), PSNR_CAP)
 
 
+def _dev_pair(gt, pred, s):
+    a = gt.pixels if isinstance(gt, Image) else gt
+    b = pred.pixels if isinstance(pred, Image) else pred
+    if tuple(a.shape) != tuple(b.shape):
+        raise InvalidInputError("image dimensions differ")
+    dev = torch.device("cuda", s.device)
+
+    def dev_t(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        return t.to(dev).contiguous()
+    ta, tb = dev_t(a), dev_t(b)
+    if ta.dtype != tb.dtype or ta.dtype not in (torch.float32, torch.float64):
+        ta, tb = ta.to(torch.float64), tb.to(torch.float64)
+    return ta, tb
+
+
+def ssim(gt, pred) -> float:
+    """ssim (metrics.py:48-65): mean SSIM of the channel-mean images, 11x11
+    Gaussian window (sigma 1.5) over valid positions; computed on the GPU."""
+    s = default_session()
+    ta, tb = _dev_pair(gt, pred, s)
+    if ta.dim() != 3 or ta.shape[2] != 3:
+        raise InvalidInputError("pixels must be (H, W, 3)")
+    H, W = int(ta.shape[0]), int(ta.shape[1])
+    if H < 11 or W < 11:
+        raise InvalidInputError("image smaller than the SSIM window")
+    out = ctypes.c_double(0.0)
+    _pre(s)
+    check(s.lib.gsv_ssim(s.handle, _ptr(ta), _ptr(tb), H, W, 1 if ta.dtype == torch.float64 else 0,
+                         ctypes.byref(out)))
+    _post(s)
+    return float(out.value)
+
+
+def d_ssim(gt, pred) -> float:
+    """d_ssim (metrics.py:68-70): (1 - SSIM) / 2."""
+    return (1.0 - ssim(gt, pred)) / 2.0
+
+
+def analyze_rd(paths, cam, gt_frames, layer: int | None = None):
+    """The measurement loop of cli.cmd_analyze (cli.py:147-162) on the GPU:
+    for each container, decode layers 1..layer, render every frame and take
+    its PSNR against gt_frames[t] without bringing images to the host.
+    Returns [(rate MB/frame, mean PSNR dB)] sorted by rate, the RdPoint
+    inputs (metrics.py:74-88)."""
+    s = default_session()
+    dev = torch.device("cuda", s.device)
+    gts = [g.to(dev) if isinstance(g, torch.Tensor) else
+           torch.from_numpy(np.ascontiguousarray(np.asarray(g.pixels if isinstance(g, Image) else g)))
+           .to(dev) for g in gt_frames]
+    c = camera_struct(cam)
+    out = torch.empty((c.height, c.width, 3), dtype=torch.float32, device=dev)
+    points = []
+    for path in paths:
+        with DeviceVideo(path, layer) as v:
+            k = v.decoded_layers
+            payload = sum(e.size for g in v.info.groups for l in range(k) for e in g.channels[l])
+            vals = []
+            for t in range(v.frame_count):
+                v.render(t, cam, out=out)
+                vals.append(psnr(gts[t], out.to(gts[t].dtype)))
+            points.append((payload / v.frame_count / 1e6, float(np.mean(vals))))
+    points.sort(key=lambda p: p[0])
+    return points
+
+
 def _atomic_write(path, blob: bytes) -> None:
     """splatio._atomic_write (splatio.py:107-117)."""
     path = Path(path)

@@ -760,6 +760,11 @@ int gsv_sqdiff(gsv_session* s, const void* a, const void* b, int64_t n, int is_f
     return GSV_OK;
 }
 
+int gsv_ssim(gsv_session* s, const void* a, const void* b, int height, int width, int is_f64, double* out) {
+    if (height < 11 || width < 11) return fail(GSV_E_INVALID_INPUT, "image smaller than the SSIM window");
+    return ssim_device(a, b, height, width, is_f64 != 0, out, s->stream);
+}
+
 int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* pos, const double* rot,
                       const double* scl, const double* opac, const double* sh, const gsv_camera* cam,
                       int32_t* rects, double* depth, int32_t* order, int32_t* tile_count,

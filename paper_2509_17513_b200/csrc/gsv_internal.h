@@ -238,6 +238,8 @@ int render_splats2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, flo
 // sum of squared differences of two device arrays (fp32 or fp64), into *out (device)
 void launch_sqdiff_f32(const float* a, const float* b, int64_t n, double* out, cudaStream_t s);
 void launch_sqdiff_f64(const double* a, const double* b, int64_t n, double* out, cudaStream_t s);
+// mean SSIM of two device (H, W, 3) images (fp32 or fp64) on stream s
+int ssim_device(const void* a, const void* b, int H, int W, bool f64, double* out_mean, cudaStream_t s);
 int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s);

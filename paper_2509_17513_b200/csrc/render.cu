@@ -636,6 +636,114 @@ void launch_sqdiff_f64(const double* a, const double* b, int64_t n, double* out,
     if (n > 0) sqdiff_kernel<double><<<(unsigned)std::max<int64_t>(g, 1), 256, 0, s>>>(a, b, n, out);
 }
 
+// ---------------------------------------------------------------------------
+// ssim (metrics.py:40-65): grayscale = channel mean, 11x11 Gaussian window
+// (sigma 1.5, normalised) over valid positions, C1 = 0.01^2, C2 = 0.03^2,
+// mean of the SSIM map.  The window is separable (outer product of the
+// normalised 1-D Gaussian), so: gray -> horizontal 1-D pass of x, y, x^2,
+// y^2, xy -> vertical pass + SSIM + block sums.  fp64 throughout.
+__constant__ double c_g11[11];
+
+template <typename T>
+__global__ void ssim_gray(const T* __restrict__ a, const T* __restrict__ b, int64_t npix,
+                          double* __restrict__ gx, double* __restrict__ gy) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += (int64_t)gridDim.x * blockDim.x) {
+        gx[i] = (((double)a[3 * i] + (double)a[3 * i + 1]) + (double)a[3 * i + 2]) / 3.0;
+        gy[i] = (((double)b[3 * i] + (double)b[3 * i + 1]) + (double)b[3 * i + 2]) / 3.0;
+    }
+}
+
+__global__ void ssim_hpass(const double* __restrict__ gx, const double* __restrict__ gy, int H, int W,
+                           double* __restrict__ h5) {
+    const int Wv = W - 10;
+    const int64_t n = (int64_t)H * Wv;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(o / Wv), j = (int)(o % Wv);
+        const double* px = gx + (size_t)i * W + j;
+        const double* py = gy + (size_t)i * W + j;
+        double s[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int v = 0; v < 11; v++) {
+            const double x = px[v], y = py[v], k = c_g11[v];
+            s[0] = fma(k, x, s[0]);
+            s[1] = fma(k, y, s[1]);
+            s[2] = fma(k, x * x, s[2]);
+            s[3] = fma(k, y * y, s[3]);
+            s[4] = fma(k, x * y, s[4]);
+        }
+#pragma unroll
+        for (int q = 0; q < 5; q++) h5[(size_t)q * n + o] = s[q];
+    }
+}
+
+__global__ void ssim_vpass(const double* __restrict__ h5, int H, int W, double* __restrict__ total) {
+    const int Wv = W - 10, Hv = H - 10;
+    const int64_t n = (int64_t)H * Wv, nv = (int64_t)Hv * Wv;
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double acc = 0.0;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nv; o += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(o / Wv), j = (int)(o % Wv);
+        double s[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < 11; u++) {
+            const size_t at = (size_t)(i + u) * Wv + j;
+            const double k = c_g11[u];
+#pragma unroll
+            for (int q = 0; q < 5; q++) s[q] = fma(k, h5[(size_t)q * n + at], s[q]);
+        }
+        const double mx = s[0], my = s[1];
+        const double vx = s[2] - mx * mx, vy = s[3] - my * my, cv = s[4] - mx * my;
+        const double num = (2 * mx * my + C1) * (2 * cv + C2);
+        const double den = (mx * mx + my * my + C1) * (vx + vy + C2);
+        acc += num / den;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) t += ws[k];
+        atomicAdd(total, t);
+    }
+}
+
+int ssim_device(const void* a, const void* b, int H, int W, bool f64, double* out_mean, cudaStream_t s) {
+    static bool init = false;
+    if (!init) {  // _ssim_kernel (metrics.py:40-45), normalised 1-D factor
+        double g[11], sum = 0;
+        for (int v = 0; v < 11; v++) {
+            const double x = v - 5.0;
+            g[v] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
+            sum += g[v];
+        }
+        for (int v = 0; v < 11; v++) g[v] /= sum;
+        GSV_CUDA(cudaMemcpyToSymbol(c_g11, g, sizeof g));
+        init = true;
+    }
+    const int64_t npix = (int64_t)H * W, nh = (int64_t)H * (W - 10);
+    double* buf = nullptr;
+    GSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)(2 * npix + 5 * nh + 1) * sizeof(double), s));
+    double* gx = buf;
+    double* gy = buf + npix;
+    double* h5 = buf + 2 * npix;
+    double* tot = h5 + 5 * nh;
+    GSV_CUDA(cudaMemsetAsync(tot, 0, sizeof(double), s));
+    const unsigned g = 148 * 8;
+    if (f64) ssim_gray<double><<<g, 256, 0, s>>>(static_cast<const double*>(a), static_cast<const double*>(b), npix, gx, gy);
+    else ssim_gray<float><<<g, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b), npix, gx, gy);
+    ssim_hpass<<<g, 256, 0, s>>>(gx, gy, H, W, h5);
+    ssim_vpass<<<g, 256, 0, s>>>(h5, H, W, tot);
+    count_launch(3);
+    double host = 0.0;
+    GSV_CUDA(cudaMemcpyAsync(&host, tot, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaFreeAsync(buf, s));
+    GSV_CUDA(cudaStreamSynchronize(s));
+    *out_mean = host / ((double)(H - 10) * (double)(W - 10));
+    return GSV_OK;
+}
+
 __global__ void copy_order(const uint32_t* __restrict__ idx0, const uint32_t* __restrict__ idx1,
                            const unsigned long long* __restrict__ ctr, int32_t* __restrict__ order,
                            const SplatRec* __restrict__ rec, int32_t* __restrict__ tile_count) {

@@ -300,7 +300,7 @@ def make_render2d(doc):
     """render(list[Splat2D]) on random projected splats (ragged rects at the
     image border, exact depth ties, negative depths, empty rects) and psnr
     values between reference images (metrics.py:31-38)."""
-    from gsv.metrics import psnr
+    from gsv.metrics import psnr, ssim
     from gsv.render import Splat2D, render
     rng = np.random.default_rng(4242)
     cam = Camera(rotation=np.eye(3), translation=np.zeros(3), fx=90.0, fy=90.0,
@@ -325,7 +325,9 @@ def make_render2d(doc):
     from gsv.render import Image as RImage
     doc["render2d"] = {"camera": cam_json(cam), "n": n,
                        "psnr_full_half": psnr(RImage(img), RImage(img_half)),
-                       "psnr_same": psnr(RImage(img), RImage(img))}
+                       "psnr_same": psnr(RImage(img), RImage(img)),
+                       "ssim_full_half": ssim(RImage(img), RImage(img_half)),
+                       "ssim_same": ssim(RImage(img), RImage(img))}
 
 
 def main():

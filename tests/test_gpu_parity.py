@@ -241,3 +241,45 @@ def test_render2d_and_psnr_gpu(gsvb):
     assert gsvb.psnr(img, img) == 99.0
     bg = gsvb.render([], cam).pixels
     assert np.array_equal(bg, np.tile(np.asarray(cam.background), (cam.height, cam.width, 1)))
+
+
+@pytest.mark.gpu
+def test_ssim_gpu(gsvb):
+    """ssim on the GPU (separable 11x11 Gaussian window, fp64) vs the
+    reference's scipy convolve2d value, fp64 and fp32 inputs."""
+    import torch
+    from golden_util import doc, renders
+    d = doc()["render2d"]
+    r = renders("render2d")
+    assert abs(gsvb.ssim(r["img"], r["img_half"]) - d["ssim_full_half"]) <= 1e-9
+    assert abs(gsvb.ssim(gsvb.Image(r["img"]), gsvb.Image(r["img"])) - 1.0) <= 1e-12
+    f32 = gsvb.ssim(torch.from_numpy(r["img"]).float().cuda(), torch.from_numpy(r["img_half"]).float().cuda())
+    assert abs(f32 - d["ssim_full_half"]) <= 1e-5
+    assert abs(gsvb.d_ssim(r["img"], r["img_half"]) - (1 - d["ssim_full_half"]) / 2) <= 1e-9
+    with pytest.raises(gsvb.InvalidInputError):
+        gsvb.ssim(np.zeros((8, 8, 3)), np.zeros((8, 8, 3)))
+
+
+@pytest.mark.gpu
+def test_analyze_rd_gpu(gsvb, tmp_path):
+    """cmd_analyze's loop (cli.py:147-162) on the GPU: decode at a layer
+    prefix, render every frame, PSNR against ground truth on the device; the
+    mean PSNR per container matches the CPU oracle's within 0.01 dB and the
+    rate is the layer-prefix payload per frame."""
+    name = "s1_rc"
+    data = container(name)
+    p = tmp_path / "c.gsv"
+    p.write_bytes(data)
+    cam = camera(name, "oblique")
+    L = doc()["scenes"][name]["layer_count"]
+    _, gt_groups = O.read_layers(data, L)
+    nfr = sum(g.frame_count for g in O.read_structure(data).groups)
+    gts = [O.render_set(O.frame_of(gt_groups, t), cam) for t in range(nfr)]
+    for k in (1, L):
+        (rate, mean_psnr), = gsvb.analyze_rd([str(p)], cam, gts, layer=k)
+        _, groups = O.read_layers(data, k)
+        ref = float(np.mean([O.psnr(gts[t], O.render_set(O.frame_of(groups, t), cam)) for t in range(nfr)]))
+        assert abs(mean_psnr - ref) <= 0.01, (k, mean_psnr, ref)
+        info = O.read_structure(data)
+        payload = sum(e.size for g in info.groups for l in range(k) for e in g.channels[l])
+        assert rate == payload / nfr / 1e6

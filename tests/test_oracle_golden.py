@@ -151,3 +151,12 @@ def test_render2d_and_psnr_oracle():
     assert O.psnr(r["img"], r["img"]) == d["psnr_same"] == 99.0
     empty = O.render2d(np.zeros((0, 2)), np.zeros((0, 2, 2)), [], np.zeros((0, 3)), [], cam)
     assert np.array_equal(empty, np.tile(np.asarray(cam.background), (cam.height, cam.width, 1)))
+
+
+def test_ssim_oracle():
+    """ssim (metrics.py:40-65) restated separably, pinned to the reference."""
+    from golden_util import doc, renders
+    d = doc()["render2d"]
+    r = renders("render2d")
+    assert abs(O.ssim(r["img"], r["img_half"]) - d["ssim_full_half"]) <= 1e-12
+    assert abs(O.ssim(r["img"], r["img"]) - d["ssim_same"]) <= 1e-12
