@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample-frames", type=int, default=2)
     p.add_argument("--streams", type=int, default=8)
+    p.add_argument("--multiview", action="store_true",
+                   help="also run BASELINE config 4's shape on this GPU: 500k Gaussians, 16 ring "
+                        "cameras, k = 1..6 (60 frames)")
     return p.parse_args()
 
 
@@ -90,6 +93,63 @@ def make_inputs(a, seed):
         tmp.write_bytes(blobs[c])
         os.replace(tmp, p)
     return blobs, key
+
+
+def ring_cameras(a, views=16):
+    """looking_at cameras on a radius-2.5 ring, 22.5 deg
+    steps, elevation +-10 deg alternating, 60 deg fov."""
+    import math
+    from paper_2509_17513_b200.types import Camera
+    cams = []
+    for v in range(views):
+        az = math.radians(22.5 * v)
+        el = math.radians(10.0 if v % 2 == 0 else -10.0)
+        eye = (2.5 * math.cos(el) * math.sin(az), 2.5 * math.sin(el), -2.5 * math.cos(el) * math.cos(az))
+        cams.append(Camera.looking_at(eye=eye, target=(0.0, 0.0, 0.0), fov_deg=60.0,
+                                      width=a.width, height=a.height, near=0.01))
+    return cams
+
+
+def run_multiview(a, sess, dev):
+    """Config 4 on one GPU: per layer prefix k, decode the container once
+    (resident in HBM) and render every frame from 16 cameras.  Metric:
+    rendered 1080p images/s (decode included)."""
+    import copy
+
+    import torch
+
+    import paper_2509_17513_b200 as gsvb
+    from paper_2509_17513_b200 import _lib
+    m = copy.copy(a)
+    m.gaussians, m.frames, m.group = 500_000, 60, 30
+    blobs, _ = make_inputs(m, 1004)
+    data = blobs[0]
+    res = torch.empty(len(data) + 64, dtype=torch.uint8, device="cuda")
+    res[:len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+    cams = [_lib.camera_struct(c) for c in ring_cameras(m)]
+    outs = [torch.empty((m.height, m.width, 3), dtype=torch.float32, device="cuda") for _ in range(m.frames)]
+    frames = list(range(m.frames))
+    out = {}
+    for k in range(1, m.layers + 1):
+        def step(verify=False):
+            v = gsvb.DeviceVideo(data, k, session=sess, resident=res)
+            for c in cams:
+                v.render_batch(frames, c, outs=outs, streams=a.streams, verify=verify)
+            v.close()
+        step(verify=True)
+        s = sess.stream
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        step()
+        e1.record(s)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        imgs = m.frames * len(cams)
+        out[str(k)] = {"images_per_s": round(imgs / (ms / 1e3), 1), "ms": round(ms, 2)}
+    return {"workload": "config4 shape on 1 GPU: 500k Gaussians, 6 layers, 60 frames (2 groups), "
+                        "16 ring cameras, 1080p, codec 0, container resident",
+            "per_layer": out}
 
 
 def camera(a):
@@ -266,6 +326,8 @@ def run_b200(a, rank, world, dist):
         e2e = {"value": round(f, 2), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(a.frames * a.width * a.height * 3)}
 
+    multiview = run_multiview(a, sess, dev) if a.multiview else None
+
     # roofline of the dominant stage (CUDA events around its launches on the
     # launching stream, one single-stream step)
     stage_ms = {k: v["ms"] for k, v in prof.items()}
@@ -291,6 +353,7 @@ def run_b200(a, rank, world, dist):
         "roofline": roof, "stages_ms_per_frame": {k: round(v["ms"] / a.frames, 5)
                                                   for k, v in prof.items()},
         "render_stats": st0, "per_layer": sweep,
+        **({"multiview": multiview} if multiview else {}),
         # whole-frame HBM roofline: algorithmic bytes of one
         # decoded+rendered frame x fps against the HBM peak
         "frame_roofline": {"bytes_per_frame": int(frame_bytes),
