@@ -177,6 +177,7 @@ struct RenderWork {
     // per tile / per pixel
     uint32_t* range = nullptr;               // [tiles][2]
     uint8_t* tile_done = nullptr;            // saturated tiles
+    uint32_t* open_mask = nullptr;           // bit per tile: still open (later rounds' emission)
     float4* state = nullptr;                 // per pixel (C.rgb, T) carried across rounds
     int64_t cap_pix = 0;
     // decoupled look-back scan state of the fused key emission

@@ -103,22 +103,35 @@ struct PlaneLoader {
         else q = __ddiv_rn((double)code, d.dir_bits >= 32 ? 4294967295.0 : (double)((1ull << d.dir_bits) - 1ull));
         return __dadd_rn(d.rmin, __dmul_rn(q, d.span));
     }
-    // slots [S0, S1): geometry (0..10) first, SH (11..) only for survivors,
-    // which keeps the SH registers out of the projection's live range
-    template <int DEG, int S0, int S1>
-    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a, const unsigned char* smem) const {
-        const double* s_q8 = reinterpret_cast<const double*>(smem);
+    // Every code of the splat is fetched first (one round of independent
+    // loads: the SH codes' latency overlaps the geometry's); geometry slots
+    // (0..10) are dequantised before the projection, SH slots (11..) only
+    // for survivors.
+    template <int DEG>
+    struct Codes {
+        uint32_t c[11 + SplatIn<DEG>::SHD];
+    };
+    template <int DEG>
+    __device__ __forceinline__ void fetch(uint32_t i, Codes<DEG>& k, const unsigned char* smem) const {
         const SlotDesc* s_sd = reinterpret_cast<const SlotDesc*>(smem + 256 * sizeof(double));
         int l = 0;
         while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
         const uint32_t j = i - src.layer_off[l];
         const SlotDesc* sd = s_sd + (size_t)l * src.nslots;
-        uint32_t code[S1 - S0];
 #pragma unroll
-        for (int s = S0; s < S1; s++) code[s - S0] = load_sample_fast(sd[s].samples, j, sd[s].bits);
+        for (int s = 0; s < 11 + SplatIn<DEG>::SHD; s++) k.c[s] = load_sample_fast(sd[s].samples, j, sd[s].bits);
+    }
+    template <int DEG, int S0, int S1>
+    __device__ __forceinline__ void load(uint32_t i, const Codes<DEG>& k, SplatIn<DEG>& a,
+                                         const unsigned char* smem) const {
+        const double* s_q8 = reinterpret_cast<const double*>(smem);
+        const SlotDesc* s_sd = reinterpret_cast<const SlotDesc*>(smem + 256 * sizeof(double));
+        int l = 0;
+        while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
+        const SlotDesc* sd = s_sd + (size_t)l * src.nslots;
 #pragma unroll
         for (int s = S0; s < S1; s++) {
-            const double v = deq(code[s - S0], sd[s], s_q8);
+            const double v = deq(k.c[s], sd[s], s_q8);
             if (s < 3) a.p[s] = v;
             else if (s < 7) a.q[s - 3] = v;
             else if (s < 10) a.s[s - 7] = v;
@@ -133,8 +146,13 @@ struct SoaLoader {
     static size_t smem_bytes(const SoaSrc&) { return 0; }
     __device__ __forceinline__ void stage(unsigned char*) const {}
     __device__ __forceinline__ int64_t count() const { return src.n; }
+    template <int DEG>
+    struct Codes {};
+    template <int DEG>
+    __device__ __forceinline__ void fetch(uint32_t, Codes<DEG>&, const unsigned char*) const {}
     template <int DEG, int S0, int S1>
-    __device__ __forceinline__ void load(uint32_t i, SplatIn<DEG>& a, const unsigned char*) const {
+    __device__ __forceinline__ void load(uint32_t i, const Codes<DEG>&, SplatIn<DEG>& a,
+                                         const unsigned char*) const {
         constexpr int shdim = SplatIn<DEG>::SHD;
         if constexpr (S0 == 0) {
 #pragma unroll
@@ -306,13 +324,15 @@ __global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
     uint64_t key = ~0ull;
     if (i < n) {
         SplatIn<DEG> a;
-        ld.template load<DEG, 0, 11>((uint32_t)i, a, proj_smem);
+        typename Loader::template Codes<DEG> codes;
+        ld.template fetch<DEG>((uint32_t)i, codes, proj_smem);
+        ld.template load<DEG, 0, 11>((uint32_t)i, codes, a, proj_smem);
         const ProjOut o = project_one(a, cam);
         alive = o.alive;
         if (dbg_depth) dbg_depth[i] = o.depth;
         if (alive) {
             key = (uint64_t)__double_as_longlong(o.depth);
-            ld.template load<DEG, 11, 11 + SplatIn<DEG>::SHD>((uint32_t)i, a, proj_smem);
+            ld.template load<DEG, 11, 11 + SplatIn<DEG>::SHD>((uint32_t)i, codes, a, proj_smem);
             double rgb[3];
             sh_color(a, cam, rgb);
             const double det = o.cov[0] * o.cov[3] - o.cov[1] * o.cov[1];

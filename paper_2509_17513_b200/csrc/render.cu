@@ -192,13 +192,37 @@ __device__ __forceinline__ unsigned long long st_pack(uint32_t epoch, uint32_t f
     return ((unsigned long long)(epoch & 0xFFFFFFu) << 40) | ((unsigned long long)flag << 38) | v;
 }
 
+// Bit t of the open-tile mask is set while tile t has a strip not yet
+// saturated (the emission of later rounds only visits those tiles).
+__global__ void open_mask_kernel(const uint32_t* __restrict__ tile_done, int ntiles, uint32_t* __restrict__ mask) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool open = t < ntiles && tile_done[t] != kTileAllSat;
+    const uint32_t b = __ballot_sync(0xffffffffu, open);
+    if ((threadIdx.x & 31) == 0 && t < ntiles) mask[t >> 5] = b;
+}
+
+// number of set bits of mask in [lo, hi] (tile ids)
+__device__ __forceinline__ uint32_t mask_count(const uint32_t* m, uint32_t lo, uint32_t hi) {
+    uint32_t c = 0;
+    for (uint32_t w = lo >> 5; w <= (hi >> 5); w++) {
+        uint32_t v = m[w];
+        if (w == (lo >> 5)) v &= 0xFFFFFFFFu << (lo & 31);
+        if (w == (hi >> 5)) v &= 0xFFFFFFFFu >> (31 - (hi & 31));
+        c += __popc(v);
+    }
+    return c;
+}
+
+constexpr int kMaskWordsSmem = 2048;  // open-tile masks of up to 65536 tiles live in shared memory
+
 __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
-    const uint32_t* __restrict__ tile_done, uint32_t* __restrict__ tkey, uint32_t* __restrict__ tval,
-    uint64_t cap, int ntx, unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
-    uint32_t epoch, uint32_t* __restrict__ ghist, int tpasses) {
+    const uint32_t* __restrict__ open_mask, int ntiles, uint32_t* __restrict__ tkey,
+    uint32_t* __restrict__ tval, uint64_t cap, int ntx, unsigned long long* __restrict__ status,
+    unsigned int* __restrict__ ticket, uint32_t epoch, uint32_t* __restrict__ ghist, int tpasses) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_hist[4][256];
+    __shared__ uint32_t s_mask[kMaskWordsSmem];
     __shared__ unsigned long long s_prefix;
     __shared__ uint32_t s_wsum[kEmitThreads / 32];
     if (threadIdx.x == 0) {
@@ -208,6 +232,12 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     }
 #pragma unroll
     for (int p = 0; p < 4; p++) s_hist[p][threadIdx.x] = 0;
+    // all tiles open (first round): open_mask == nullptr
+    const int nwords = (ntiles + 31) >> 5;
+    const bool mask_in_smem = open_mask && nwords <= kMaskWordsSmem;
+    if (mask_in_smem)
+        for (int w = threadIdx.x; w < nwords; w += kEmitThreads) s_mask[w] = open_mask[w];
+    const uint32_t* mask = mask_in_smem ? s_mask : open_mask;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t nvis = (uint32_t)ctr[C_NVIS];
@@ -221,22 +251,22 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         }
         return;
     }
-    const uint32_t base = tile * kEmitTile + threadIdx.x * kEmitPer;
-    uint32_t cnt[kEmitPer];
+    static_assert(kEmitPer == 1, "one splat per thread");
+    const uint32_t base = tile * kEmitTile + threadIdx.x;
+    uint32_t x0 = 1, x1 = 0, y0 = 1, y1 = 0;  // this thread's splat, tile coordinates (inclusive)
     uint32_t sum = 0;
-#pragma unroll
-    for (int k = 0; k < kEmitPer; k++) {
-        cnt[k] = 0;
-        if (base + k < m) {
-            const SplatRec s = rec_sorted[a + base + k];
-            const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
-            const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
-            uint32_t c = 0;
-            for (uint32_t ty = y0; ty <= y1; ty++)
-                for (uint32_t tx = x0; tx <= x1; tx++) c += tile_done[ty * ntx + tx] == kTileAllSat ? 0u : 1u;
-            cnt[k] = c;
+    if (base < m) {
+        const SplatRec* sr = rec_sorted + a + base;
+        const uint2 r = make_uint2(__ldg(&sr->rx), __ldg(&sr->ry));
+        x0 = (r.x & 0xFFFFu) / kTile;
+        x1 = ((r.x >> 16) - 1) / kTile;
+        y0 = (r.y & 0xFFFFu) / kTile;
+        y1 = ((r.y >> 16) - 1) / kTile;
+        if (!mask) {
+            sum = (x1 - x0 + 1) * (y1 - y0 + 1);
+        } else {
+            for (uint32_t ty = y0; ty <= y1; ty++) sum += mask_count(mask, ty * ntx + x0, ty * ntx + x1);
         }
-        sum += cnt[k];
     }
     // block exclusive scan of the per-thread sums
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -296,18 +326,14 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         }
     }
     __syncthreads();
-    unsigned long long o = s_prefix + excl;
-#pragma unroll
-    for (int k = 0; k < kEmitPer; k++) {
-        if (base + k >= m || cnt[k] == 0) continue;
-        const uint32_t r = a + base + k;
-        const SplatRec s = rec_sorted[r];
-        const uint32_t x0 = (s.rx & 0xFFFFu) / kTile, x1 = ((s.rx >> 16) - 1) / kTile;
-        const uint32_t y0 = (s.ry & 0xFFFFu) / kTile, y1 = ((s.ry >> 16) - 1) / kTile;
+    // scatter this thread's splat's keys in rank order (open tiles only)
+    if (sum) {
+        unsigned long long o = s_prefix + excl;
+        const uint32_t r = a + base;
         for (uint32_t ty = y0; ty <= y1; ty++)
             for (uint32_t tx = x0; tx <= x1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
-                if (tile_done[t] == kTileAllSat) continue;
+                if (mask && !((mask[t >> 5] >> (t & 31)) & 1u)) continue;
                 if (o < cap) {
                     tkey[o] = t;
                     tval[o] = r;
@@ -349,6 +375,7 @@ void work_free(RenderWork* w) {
     free_ptr(w->range);
     free_ptr(w->state);
     free_ptr(w->tile_done);
+    free_ptr(w->open_mask);
     free_ptr(w->status);
     free_ptr(w->sort_ghist);
     free_ptr(w->sort_status);
@@ -400,8 +427,10 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
     if (tiles > w->cap_tiles) {
         free_ptr(w->range);
         free_ptr(w->tile_done);
+        free_ptr(w->open_mask);
         GSV_CUDA(cudaMalloc(&w->range, (size_t)tiles * 2 * sizeof(uint32_t)));
         GSV_CUDA(cudaMalloc(&w->tile_done, (size_t)tiles * 4));
+        GSV_CUDA(cudaMalloc(&w->open_mask, ((size_t)tiles + 31) / 32 * 4 + 4));
         w->cap_tiles = tiles;
     }
     if (npix > w->cap_pix) {
@@ -533,8 +562,14 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         prof_mark(ST_EMIT, s);
         const unsigned ge = std::max(1u, (unsigned)((b - a + kEmitTile - 1) / kEmitTile));
         uint32_t* th = sc.ghist + 1024 * (1 + (int)std::min<size_t>(j, kHistRegions - 2));
-        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b,
-                                                      reinterpret_cast<const uint32_t*>(w->tile_done), w->tkey[0],
+        uint32_t* mask = nullptr;  // first round: every tile open
+        if (j > 0) {
+            mask = w->open_mask;
+            open_mask_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(w->tile_done),
+                                                                  ntiles, mask);
+            count_launch(1);
+        }
+        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b, mask, ntiles, w->tkey[0],
                                                       w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
                                                       w->ticket, ++w->epoch, th, tp);
         count_launch(1);
