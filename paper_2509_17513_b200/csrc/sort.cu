@@ -70,7 +70,10 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_wcnt[kThreads / 32][kRadix];
     __shared__ uint32_t s_dbase[kRadix];
+    __shared__ uint32_t s_lbase[kRadix];
     __shared__ uint32_t s_wsum[kThreads / 32];
+    __shared__ K s_k[kTileItems];
+    __shared__ uint32_t s_v[kTileItems];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) {
         const uint32_t tk = atomicAdd(ticket, 1u);
@@ -160,14 +163,38 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
         atomicExch(status + (size_t)tile * kRadix + t, os_pack(epoch, 2, prefix + tot));
     }
     s_dbase[t] = gbase + prefix;
+    // tile-local digit bases (exclusive scan of the digit totals), then the
+    // keys are staged in shared memory in digit order so the global writes of
+    // each digit's run are coalesced
+    uint32_t lx = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, lx, o);
+        if (lane >= o) lx += y;
+    }
+    __syncthreads();  // s_wsum reuse
+    if (lane == 31) s_wsum[warp] = lx;
+    __syncthreads();
+    uint32_t lb = lx - tot;
+    for (int w = 0; w < warp; w++) lb += s_wsum[w];
+    s_lbase[t] = lb;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kItems; i++) {
         if (d[i] < kRadix) {
-            const uint32_t pos = s_dbase[d[i]] + s_wcnt[warp][d[i]] + r[i];
-            kout[pos] = k[i];
-            vout[pos] = v[i];
+            const uint32_t lp = s_lbase[d[i]] + s_wcnt[warp][d[i]] + r[i];
+            s_k[lp] = k[i];
+            s_v[lp] = v[i];
         }
+    }
+    __syncthreads();
+    const uint32_t valid = min((uint32_t)kTileItems, n - tile * kTileItems);
+    for (uint32_t i = t; i < valid; i += kThreads) {
+        const K key = s_k[i];
+        const uint32_t dg = (uint32_t)(key >> shift) & 0xFFu;
+        const uint32_t pos = s_dbase[dg] + (i - s_lbase[dg]);
+        kout[pos] = key;
+        vout[pos] = s_v[i];
     }
 }
 
