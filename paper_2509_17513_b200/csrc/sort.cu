@@ -75,13 +75,6 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
     __shared__ K s_k[kTileItems];
     __shared__ uint32_t s_v[kTileItems];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    if (t == 0) {
-        const uint32_t tk = atomicAdd(ticket, 1u);
-        if (tk == gridDim.x - 1) *ticket = 0;  // every CTA has its ticket: reset for the next pass
-        s_tile = tk;
-    }
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; w++) s_wcnt[w][t] = 0;
     // exclusive scan of this pass's global digit counts
     const uint32_t gv = ghist[pass * kRadix + t];
     uint32_t gx = gv;
@@ -94,9 +87,21 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
     __syncthreads();
     uint32_t gbase = gx - gv;
     for (int w = 0; w < warp; w++) gbase += s_wsum[w];
-    const uint32_t tile = s_tile;
     const uint32_t n = (uint32_t)*n_ptr;
     const uint32_t ntiles = (n + kTileItems - 1) / kTileItems;
+    // persistent CTAs take tiles in ticket order until none is left; every
+    // CTA ends with one ticket past the end, so the last of those resets
+    for (;;) {
+    __syncthreads();
+    if (t == 0) {
+        const uint32_t tk = atomicAdd(ticket, 1u);
+        if (tk == ntiles + gridDim.x - 1) *ticket = 0;
+        s_tile = tk;
+    }
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; w++) s_wcnt[w][t] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
     const int shift = 8 * pass;
     const uint32_t base = tile * kTileItems + warp * (32 * kItems) + lane;
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
         kout[pos] = key;
         vout[pos] = s_v[i];
     }
+    }  // next tile
 }
 
 template <typename K>
@@ -203,7 +209,7 @@ void radix_sort(K* keys[2], uint32_t* vals[2], const unsigned long long* n_ptr, 
                 int npasses_max, const int* npasses_dev, uint32_t* ghist, const SortScratch& sc,
                 cudaStream_t s) {
     const int64_t tiles = (cap + kTileItems - 1) / kTileItems;
-    const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 2));
     if (!ghist) {  // histograms not provided by the producer of the keys
         ghist = sc.ghist;
         cudaMemsetAsync(ghist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s);
