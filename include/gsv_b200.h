@@ -122,6 +122,10 @@ int gsv_video_open(gsv_session* s, const uint8_t* data, size_t len, int up_to_la
                    gsv_video** out);
 int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len,
                             const uint8_t* dev_data, int up_to_layer, gsv_video** out);
+/* groups [g0, g1) only (a streaming player's unit): only their layer-prefix
+ * bytes are staged and decoded; frames are numbered 0.. within the range. */
+int gsv_video_open_groups(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer, int g0,
+                          int g1, gsv_video** out);
 void gsv_video_close(gsv_video* v);
 int gsv_video_frame_count(const gsv_video* v);
 int gsv_video_decoded_layers(const gsv_video* v);

@@ -75,6 +75,7 @@ _SIGS = {
     "gsv_read_group": (_I, [_P, _SZ, _I, ctypes.POINTER(GroupInfo_t)]),
     "gsv_read_entry": (_I, [_P, _SZ, _I, _I, _I, ctypes.POINTER(EntryInfo_t)]),
     "gsv_video_open": (_I, [_P, _P, _SZ, _I, ctypes.POINTER(_P)]),
+    "gsv_video_open_groups": (_I, [_P, _P, _SZ, _I, _I, _I, ctypes.POINTER(_P)]),
     "gsv_video_open_resident": (_I, [_P, _P, _SZ, _P, _I, ctypes.POINTER(_P)]),
     "gsv_video_close": (None, [_P]),
     "gsv_video_frame_count": (_I, [_P]),

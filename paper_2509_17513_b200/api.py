@@ -49,7 +49,9 @@ class Session:
             raise RuntimeError("paper_2509_17513_b200 needs a CUDA device (B200); none is visible")
         L = _lib.load()
         self.device = torch.cuda.current_device() if device is None else int(device)
-        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        # high priority: a container open's upload / decode / CRC kernels get
+        # SMs ahead of frame rendering on the auxiliary streams
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device, priority=-1)
         h = ctypes.c_void_p()
         check(L.gsv_session_create(self.device, self.stream.cuda_stream, ctypes.byref(h)))
         self.handle = h
@@ -213,7 +215,11 @@ class DeviceVideo:
     """
 
     def __init__(self, source, up_to_layer: int | None = None, session: Session | None = None,
-                 resident: torch.Tensor | None = None):
+                 resident: torch.Tensor | None = None, groups: tuple | None = None,
+                 info: ContainerInfo | None = None):
+        """groups=(g0, g1): open only those groups (a streaming player's
+        unit; only their bytes are staged and decoded, frames numbered from 0
+        within the range)."""
         self.session = session or default_session()
         L = self.session.lib
         ptr = None
@@ -224,7 +230,7 @@ class DeviceVideo:
             src = source.contiguous()
             ptr, n = src.data_ptr(), src.numel()
             want = 1 << 16
-            while True:
+            while info is None:
                 head = bytes(src[:min(n, want)].numpy())
                 try:
                     info = _structure_from_bytes(head)
@@ -253,7 +259,17 @@ class DeviceVideo:
         _pre(self.session)
         nbytes = data.numel() if ptr is not None else len(data)
         hptr = ptr if ptr is not None else data
-        if resident is not None:
+        self.group_range = None
+        if groups is not None:
+            g0, g1 = int(groups[0]), int(groups[1])
+            if resident is not None:
+                raise InvalidInputError("groups= needs a host source")
+            check(L.gsv_video_open_groups(self.session.handle, hptr, nbytes, k, g0, g1, ctypes.byref(h)))
+            self.group_range = (g0, g1)
+            info = ContainerInfo(info.version, info.layer_count, info.sh_degree, info.fps, info.bounds,
+                                 info.flags, tuple(info.groups[g0:g1]))
+            self.info = info
+        elif resident is not None:
             check(L.gsv_video_open_resident(self.session.handle, hptr, nbytes,
                                             resident.data_ptr(), k, ctypes.byref(h)))
         else:
@@ -380,8 +396,10 @@ class DeviceVideo:
     def to_decoded_video(self) -> DecodedVideo:
         groups = []
         k = self.decoded_layers
+        local = 0  # frames are numbered from 0 within the opened groups
         for g in self.info.groups:
-            frames = tuple(self.frame(g.start_frame + i) for i in range(g.frame_count))
+            frames = tuple(self.frame(local + i) for i in range(g.frame_count))
+            local += g.frame_count
             groups.append(DecodedGroup(g.start_frame, g.frame_count, tuple(g.layer_counts[:k]),
                                        frames))
         return DecodedVideo(self.info.layer_count, k, self.info.sh_degree, self.info.fps,

@@ -32,8 +32,14 @@ struct gsv_session {
     // frame overlap with other frames' kernels
     std::vector<cudaStream_t> aux;
     std::vector<RenderWork*> aux_work;
-    std::vector<uint8_t*> aux_u8;  // staging for host u8 outputs
+    std::vector<uint8_t*> aux_u8;  // staging for host u8 outputs: 2 buffers per aux stream
     std::vector<size_t> aux_u8_cap;
+    // read-back of host u8 outputs: per aux stream a copy stream, and per
+    // staging buffer "rendered" / "copied" events, so the D2H of frame j
+    // overlaps the rendering of frame j+1 on the same aux stream
+    std::vector<cudaStream_t> aux_copy;
+    std::vector<cudaEvent_t> ev_rendered, ev_copied, ev_copy_join;
+    std::vector<int> aux_flip;
     cudaEvent_t ev_fork = nullptr;
     std::vector<cudaEvent_t> ev_join;
     int64_t kcap_hint = 0;
@@ -104,11 +110,54 @@ struct DevBuf {
     }
 };
 
+// Pinned host staging for the small descriptor uploads and read-backs of a
+// container open: a pageable cudaMemcpyAsync is synchronous and queues behind
+// the big transfers other streams have in flight (frame read-backs, other
+// groups' payload uploads), so the open's small copies go through this
+// per-thread pinned bump buffer instead.  reset() at the start of an open
+// (the previous open synchronised before returning).
+struct PinnedStage {
+    uint8_t* p = nullptr;
+    size_t cap = 0, used = 0;
+    ~PinnedStage() {
+        if (p) cudaFreeHost(p);
+    }
+    void reset() { used = 0; }
+    uint8_t* reserve(size_t n, cudaStream_t s) {
+        const size_t need = ((used + 255) & ~size_t(255)) + n;
+        if (need > cap) {  // grow: drain in-flight copies from the old buffer first
+            cudaStreamSynchronize(s);
+            if (p) cudaFreeHost(p);
+            cap = std::max(need * 2, (size_t)1 << 20);
+            p = nullptr;
+            if (cudaMallocHost(reinterpret_cast<void**>(&p), cap) != cudaSuccess) {
+                p = nullptr;
+                cap = 0;
+                return nullptr;
+            }
+            used = 0;
+        }
+        used = (used + 255) & ~size_t(255);
+        uint8_t* q = p + used;
+        used += n;
+        return q;
+    }
+};
+thread_local PinnedStage t_stage;
+
 template <class T>
 int upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
     int rc = b.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
     if (rc) return rc;
-    if (!v.empty()) GSV_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (v.empty()) return GSV_OK;
+    const size_t n = v.size() * sizeof(T);
+    uint8_t* h = t_stage.reserve(n, s);
+    if (h) {
+        memcpy(h, v.data(), n);
+        GSV_CUDA(cudaMemcpyAsync(b.p, h, n, cudaMemcpyHostToDevice, s));
+    } else {
+        GSV_CUDA(cudaMemcpyAsync(b.p, v.data(), n, cudaMemcpyHostToDevice, s));
+    }
     return GSV_OK;
 }
 
@@ -304,9 +353,12 @@ struct RunSet {
         if (chunk_prefix.back()) count_launch();
         prof_mark(ST_COUNT, s);
         crc.assign(runs.size(), 0);
+        uint32_t* hcrc = runs.empty() ? nullptr : reinterpret_cast<uint32_t*>(t_stage.reserve(runs.size() * 4, s));
         if (!runs.empty())
-            GSV_CUDA(cudaMemcpyAsync(crc.data(), d_crc.p, runs.size() * 4, cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaMemcpyAsync(hcrc ? (void*)hcrc : (void*)crc.data(), d_crc.p, runs.size() * 4,
+                                     cudaMemcpyDeviceToHost, s));
         GSV_CUDA(cudaStreamSynchronize(s));
+        if (hcrc) memcpy(crc.data(), hcrc, runs.size() * 4);
         GSV_CUDA(cudaGetLastError());
         return GSV_OK;
     }
@@ -330,8 +382,9 @@ struct gsv_video {
 namespace {
 
 int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
-               int up_to_layer, gsv_video** out) {
+               int up_to_layer, gsv_video** out, int g0 = 0, int g1 = -1) {
     *out = nullptr;
+    t_stage.reset();
     gsv_video* v = new gsv_video();
     v->s = s;
     auto bail = [&](int rc) {
@@ -340,6 +393,16 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     };
     int rc = parse_container(data, len, &v->c);
     if (rc) return bail(rc);
+    if (g1 == -1) g1 = (int)v->c.groups.size();
+    if (g0 < 0 || g1 > (int)v->c.groups.size() || g0 >= g1)
+        return bail(fail(GSV_E_INVALID_INPUT, "group range [" + std::to_string(g0) + ", " + std::to_string(g1) +
+                                                  ") out of range 0.." + std::to_string(v->c.groups.size())));
+    if (g0 > 0 || g1 < (int)v->c.groups.size()) {  // keep the selected groups only (their bytes only are staged)
+        v->c.groups.erase(v->c.groups.begin() + g1, v->c.groups.end());
+        v->c.groups.erase(v->c.groups.begin(), v->c.groups.begin() + g0);
+        const uint32_t base = v->c.groups[0].start_frame;  // frames numbered from 0 in the range
+        for (GroupDir& gd : v->c.groups) gd.start_frame -= base;
+    }
     const Container& c = v->c;
     const int L = c.layer_count;
     const int k = up_to_layer == -1 ? L : up_to_layer;
@@ -556,11 +619,18 @@ void gsv_session_destroy(gsv_session* s) {
     cudaStreamSynchronize(s->stream);
     for (size_t i = 0; i < s->aux.size(); i++) {
         cudaStreamSynchronize(s->aux[i]);
+        cudaStreamSynchronize(s->aux_copy[i]);
         work_free(s->aux_work[i]);
         delete s->aux_work[i];
-        if (s->aux_u8[i]) cudaFree(s->aux_u8[i]);
+        for (int b = 0; b < 2; b++) {
+            if (s->aux_u8[2 * i + b]) cudaFree(s->aux_u8[2 * i + b]);
+            cudaEventDestroy(s->ev_rendered[2 * i + b]);
+            cudaEventDestroy(s->ev_copied[2 * i + b]);
+        }
         cudaStreamDestroy(s->aux[i]);
+        cudaStreamDestroy(s->aux_copy[i]);
         cudaEventDestroy(s->ev_join[i]);
+        cudaEventDestroy(s->ev_copy_join[i]);
     }
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     work_free(&s->work);
@@ -594,6 +664,12 @@ int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len, con
     GSV_CUDA(cudaSetDevice(s->device));
     if (!dev_data) return fail(GSV_E_INVALID_INPUT, "dev_data is NULL");
     return open_video(s, data, len, dev_data, up_to_layer, out);
+}
+
+int gsv_video_open_groups(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer, int g0, int g1,
+                          gsv_video** out) {
+    GSV_CUDA(cudaSetDevice(s->device));
+    return open_video(s, data, len, nullptr, up_to_layer, out, g0, g1);
 }
 
 void gsv_video_close(gsv_video* v) {
@@ -662,9 +738,24 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
         GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         s->aux.push_back(st);
         s->aux_work.push_back(new RenderWork());
-        s->aux_u8.push_back(nullptr);
-        s->aux_u8_cap.push_back(0);
         s->ev_join.push_back(e);
+        cudaStream_t cs;
+        GSV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        s->aux_copy.push_back(cs);
+        cudaEvent_t cj;
+        GSV_CUDA(cudaEventCreateWithFlags(&cj, cudaEventDisableTiming));
+        s->ev_copy_join.push_back(cj);
+        s->aux_flip.push_back(0);
+        for (int b = 0; b < 2; b++) {
+            s->aux_u8.push_back(nullptr);
+            s->aux_u8_cap.push_back(0);
+            cudaEvent_t er, ec;
+            GSV_CUDA(cudaEventCreateWithFlags(&er, cudaEventDisableTiming));
+            GSV_CUDA(cudaEventCreateWithFlags(&ec, cudaEventDisableTiming));
+            GSV_CUDA(cudaEventRecord(ec, cs));  // buffer free
+            s->ev_rendered.push_back(er);
+            s->ev_copied.push_back(ec);
+        }
     }
     if (!s->ev_fork) GSV_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     const CamDev cd = make_cam(*cam);
@@ -676,10 +767,14 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
                 int rc = work_reserve(s->aux_work[i], 1, khint, 0, 0);
                 if (rc) return rc;
             }
-            if (host_rgb8 && s->aux_u8_cap[i] < img8) {
-                if (s->aux_u8[i]) cudaFree(s->aux_u8[i]);
-                GSV_CUDA(cudaMalloc(&s->aux_u8[i], img8));
-                s->aux_u8_cap[i] = img8;
+            for (int b = 0; b < 2 && host_rgb8; b++) {
+                const int q = 2 * i + b;
+                if (s->aux_u8_cap[q] < img8) {
+                    GSV_CUDA(cudaStreamSynchronize(s->aux_copy[i]));
+                    if (s->aux_u8[q]) cudaFree(s->aux_u8[q]);
+                    GSV_CUDA(cudaMalloc(&s->aux_u8[q], img8));
+                    s->aux_u8_cap[q] = img8;
+                }
             }
         }
         GSV_CUDA(cudaEventRecord(s->ev_fork, s->stream));
@@ -691,15 +786,30 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
             if (rc) return rc;
             uint8_t* o8 = out_rgb8 ? out_rgb8[j] : nullptr;
             const bool to_host = host_rgb8 && host_rgb8[j];
-            if (to_host) o8 = s->aux_u8[i];
+            int q = 0;
+            if (to_host) {
+                q = 2 * i + s->aux_flip[i];
+                s->aux_flip[i] ^= 1;
+                GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_copied[q], 0));  // staging buffer free
+                o8 = s->aux_u8[q];
+            }
             rc = render_planes(src, cd, s->aux_work[i], out_rgb ? out_rgb[j] : nullptr, o8,
                                reinterpret_cast<gsv_render_stats*>(1), s->aux[i]);
             if (rc) return rc;
-            if (to_host) GSV_CUDA(cudaMemcpyAsync(host_rgb8[j], o8, img8, cudaMemcpyDeviceToHost, s->aux[i]));
+            if (to_host) {
+                GSV_CUDA(cudaEventRecord(s->ev_rendered[q], s->aux[i]));
+                GSV_CUDA(cudaStreamWaitEvent(s->aux_copy[i], s->ev_rendered[q], 0));
+                GSV_CUDA(cudaMemcpyAsync(host_rgb8[j], o8, img8, cudaMemcpyDeviceToHost, s->aux_copy[i]));
+                GSV_CUDA(cudaEventRecord(s->ev_copied[q], s->aux_copy[i]));
+            }
         }
         for (int i = 0; i < nstreams; i++) {
             GSV_CUDA(cudaEventRecord(s->ev_join[i], s->aux[i]));
             GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join[i], 0));
+            if (host_rgb8) {
+                GSV_CUDA(cudaEventRecord(s->ev_copy_join[i], s->aux_copy[i]));
+                GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_copy_join[i], 0));
+            }
         }
         if (!check) return GSV_OK;
         GSV_CUDA(cudaStreamSynchronize(s->stream));

@@ -283,3 +283,27 @@ def test_analyze_rd_gpu(gsvb, tmp_path):
         info = O.read_structure(data)
         payload = sum(e.size for g in info.groups for l in range(k) for e in g.channels[l])
         assert rate == payload / nfr / 1e6
+
+
+@pytest.mark.gpu
+def test_open_group_range(gsvb):
+    """gsv_video_open_groups: a group range decodes exactly like those groups
+    of the whole container (frames numbered from 0 in the range)."""
+    name = "s1_rc"
+    data = container(name)
+    info = O.read_structure(data)
+    G = len(info.groups)
+    assert G >= 2
+    k = doc()["scenes"][name]["layer_count"]
+    _, groups = O.read_layers(data, k)
+    start = 0
+    for g in range(G):
+        with gsvb.DeviceVideo(data, k, groups=(g, g + 1)) as v:
+            assert v.frame_count == info.groups[g].frame_count
+            for i in range(v.frame_count):
+                got, ref = v.frame(i), O.frame_of(groups, start + i)
+                for nm in ("positions", "rotations", "scales", "opacities", "sh"):
+                    assert np.array_equal(getattr(got, nm), getattr(ref, nm)), (g, i, nm)
+        start += info.groups[g].frame_count
+    with pytest.raises(gsvb.InvalidInputError):
+        gsvb.DeviceVideo(data, k, groups=(G, G + 1))
