@@ -180,17 +180,23 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
         const int cnt = (int)min(32u, end - base);
         for (int q = 0; q < cnt; q++) {
             const uint32_t ra = sbase + (uint32_t)q * 64u;
-            const float4 rc = lds_f4(ra);  // x0, y0, x1, y1 (exact integers)
+            const float4 rc = lds_f4(ra);        // x0, y0, x1, y1 as floats (exact integers)
+            const float4 r3 = lds_f4(ra + 48u);  // op, rx = x0 | x1 << 16, ry = y0 | y1 << 16
+            const uint32_t rx = __float_as_uint(r3.y), ry = __float_as_uint(r3.z);
+            const int y0 = (int)(ry & 0xFFFFu), y1 = (int)(ry >> 16);
             // strip rows [sy0, sy0 + 2 ROWS) against [y0, y1): warp-uniform skip
-            if (rc.y >= (float)(sy0 + 2 * ROWS) || rc.w <= (float)sy0) continue;
-            // rows of the lane's column inside the rect (empty outside its columns)
-            const bool colin = pxf >= rc.x && pxf < rc.z;
-            const int lo = min(max((int)rc.y - py0, 0), ROWS), hi = min(max((int)rc.w - py0, 0), ROWS);
+            // (a strip of 8-row lanes is the whole tile: every record overlaps it)
+            if (kStrips > 1 && (y0 >= sy0 + 2 * ROWS || y1 <= sy0)) continue;
+            // rows of the lane's column inside the rect (empty outside its columns);
+            // integer rect from the record: no float->int conversions on the
+            // SFU pipe the ex2s need
+            const bool colin = px >= (int)(rx & 0xFFFFu) && px < (int)(rx >> 16);
+            const int lo = min(max(y0 - py0, 0), ROWS), hi = min(max(y1 - py0, 0), ROWS);
             const uint32_t m = colin ? ((0xFFFFu << lo) & ~(0xFFFFu << hi)) : 0u;
             if (!__any_sync(0xffffffffu, m & live)) continue;  // converged: lanes mask, not branch
             const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
-            const float op = lds_f4(ra + 48u).x;
+            const float op = r3.x;
             const float dx = (pxf - rc.x) - a.x;
             const float A = a.z * dx * dx, B = a.w * dx;
             const float dy0 = (py0f - rc.y) - a.y;

@@ -507,6 +507,22 @@ static void round_bounds(int64_t n, std::vector<uint32_t>* b) {
 // Dev diagnostics: GSV_DEBUG_SKIP lists stages whose kernels are not
 // launched (composite, tsort, dsort, emit) -- wrong images, used only to
 // measure what each stage costs in the frame-parallel steady state.
+static unsigned debug_double() {  // GSV_DEBUG_DOUBLE: stages launched twice (marginal cost probe)
+    static int init = 0;
+    static unsigned mask = 0;
+    if (!init) {
+        if (const char* e = getenv("GSV_DEBUG_DOUBLE")) {
+            if (strstr(e, "composite")) mask |= 1;
+            if (strstr(e, "tsort")) mask |= 2;
+            if (strstr(e, "dsort")) mask |= 4;
+            if (strstr(e, "emit")) mask |= 8;
+            if (strstr(e, "project")) mask |= 16;
+        }
+        init = 1;
+    }
+    return mask;
+}
+
 static unsigned debug_skip() {
     static int init = 0;
     static unsigned mask = 0;
@@ -540,13 +556,15 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     prof_mark(ST_PROJECT, s);
     reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, reinterpret_cast<uint32_t*>(w->tile_done),
                                           ntiles, open_word(composite_rows()));
-    const unsigned skip = debug_skip();
+    const unsigned skip = debug_skip(), dbl = debug_double();
     if (!(skip & 16)) project();
+    if (dbl & 16) project();
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
         depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
         if (!(skip & 4)) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
+        if (dbl & 4) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         count_launch(2 + radix_launches(4, true));
     }
@@ -575,8 +593,12 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         count_launch(1);
         prof_mark(ST_TSORT, s);
         if (!(skip & 2)) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
+        if (dbl & 2) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
         count_launch(radix_launches(tp, true));
         prof_mark(ST_COMPOSITE, s);
+        if ((dbl & 1) && j == 0)
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+                                   w->tile_done, cam, true, false, out_rgb, out_rgb8, s);
         if (!(skip & 1))
             launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
                                    w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
