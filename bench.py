@@ -66,6 +66,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample-frames", type=int, default=2)
     p.add_argument("--streams", type=int, default=8)
+    p.add_argument("--short-groups", action="store_true",
+                   help="also time both codecs with config 3's grouping (a burst every 2 frames: "
+                        "150 motion groups) at config 2's size")
     p.add_argument("--multiview", action="store_true",
                    help="also run BASELINE config 4's shape on this GPU: 500k Gaussians, 16 ring "
                         "cameras, k = 1..6 (60 frames)")
@@ -126,6 +129,7 @@ def run_multiview(a, sess, dev):
     m.gaussians, m.frames, m.group = 500_000, 60, 30
     blobs, _ = make_inputs(m, 1004)
     data = blobs[0]
+    dinfo = gsvb.read_structure(data)  # the directory, parsed once per container
     res = torch.empty(len(data) + 64, dtype=torch.uint8, device="cuda")
     res[:len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
     cams = [_lib.camera_struct(c) for c in ring_cameras(m)]
@@ -134,7 +138,7 @@ def run_multiview(a, sess, dev):
     out = {}
     for k in range(1, m.layers + 1):
         def step(verify=False):
-            v = gsvb.DeviceVideo(data, k, session=sess, resident=res)
+            v = gsvb.DeviceVideo(data, k, session=sess, resident=res, info=dinfo)
             for c in cams:
                 v.render_batch(frames, c, outs=outs, streams=a.streams, verify=verify)
             v.close()
@@ -152,6 +156,50 @@ def run_multiview(a, sess, dev):
     return {"workload": "config4 shape on 1 GPU: 500k Gaussians, 6 layers, 60 frames (2 groups), "
                         "16 ring cameras, 1080p, codec 0, container resident",
             "per_layer": out}
+
+
+def run_short_groups(a, sess):
+    """Config 3's adaptive grouping (2-frame motion groups, bursts every 2
+    frames) at config 2's size: the range decoder's serial chain per run is
+    1 plane long instead of 29, and 150 groups decode in parallel.  Same step
+    as the headline (open + decode + CRC + render of all frames, container
+    resident), both codecs, k = 6."""
+    import copy
+
+    import torch
+
+    import paper_2509_17513_b200 as gsvb
+    from paper_2509_17513_b200 import _lib
+    m = copy.copy(a)
+    m.group = 2
+    blobs, _ = make_inputs(m, 1003)
+    cs = _lib.camera_struct(camera(m))
+    outs = [torch.empty((m.height, m.width, 3), dtype=torch.float32, device="cuda") for _ in range(m.frames)]
+    res = {}
+    for codec in (0, 1):
+        data = blobs[codec]
+        dinfo = gsvb.read_structure(data)  # the directory, parsed once per container
+        dev = torch.empty(len(data) + 64, dtype=torch.uint8, device="cuda")
+        dev[:len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+
+        def step(verify=False):
+            v = gsvb.DeviceVideo(data, m.layers, session=sess, resident=dev, info=dinfo)
+            v.render_batch(list(range(m.frames)), cs, outs=outs, streams=a.streams, verify=verify)
+            v.close()
+        step(verify=True)
+        s = sess.stream
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(2):
+            step()
+        e1.record(s)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / 2
+        res[f"codec{codec}"] = {"fps": round(m.frames / (ms / 1e3), 1), "ms_per_step": round(ms, 2),
+                                "container_mb": round(len(data) / 1e6, 1)}
+    return {"workload": "config3 grouping at config2 size: 300k Gaussians, 6 layers, 300 frames in "
+                        "150 two-frame motion groups, 1080p, k = 6, container resident", **res}
 
 
 def camera(a):
@@ -223,6 +271,7 @@ def run_b200(a, rank, world, dist):
     sess = gsvb.Session(dev)
     s = sess.stream
     resident = {}
+    infos = {c: gsvb.read_structure(b) for c, b in blobs.items()}  # directories, parsed once
     for c, b in blobs.items():
         t = torch.empty(len(b) + 64, dtype=torch.uint8, device="cuda")
         t[:len(b)].copy_(torch.frombuffer(bytearray(b), dtype=torch.uint8))
@@ -234,13 +283,14 @@ def run_b200(a, rank, world, dist):
     frames = list(range(a.frames))
 
     def step_resident(codec, k, verify=False, streams=None):
-        v = gsvb.DeviceVideo(blobs[codec], k, session=sess, resident=resident[codec])
+        v = gsvb.DeviceVideo(blobs[codec], k, session=sess, resident=resident[codec], info=infos[codec])
         v.render_batch(frames, cs, outs=outs, streams=streams or a.streams, verify=verify)
         return v
 
     # size the key buffers (stats path + one checked batch per codec)
     for codec in (0, 1):
-        v = gsvb.DeviceVideo(blobs[codec], a.layers, session=sess, resident=resident[codec])
+        v = gsvb.DeviceVideo(blobs[codec], a.layers, session=sess, resident=resident[codec],
+                             info=infos[codec])
         _, st0 = v.render(0, cam, stats=True)
         v.close()
         step_resident(codec, a.layers, verify=True).close()
@@ -257,7 +307,7 @@ def run_b200(a, rank, world, dist):
         def one(verify=False):
             if not e2e:
                 return step_resident(codec, k, verify=verify)
-            v = gsvb.DeviceVideo(host, k, session=sess)
+            v = gsvb.DeviceVideo(host, k, session=sess, info=infos[codec])
             v.render_batch(frames, cs, host_u8=host_frames, streams=a.streams, verify=verify)
             return v
 
@@ -333,6 +383,7 @@ def run_b200(a, rank, world, dist):
                "pcie_floor_ms_per_step": "H2D 42 + D2H 34 concurrently 51 (tools/pcie_probe.py)"}
 
     multiview = run_multiview(a, sess, dev) if a.multiview else None
+    short_groups = run_short_groups(a, sess) if a.short_groups else None
 
     # roofline of the dominant stage (CUDA events around its launches on the
     # launching stream, one single-stream step)
@@ -360,6 +411,7 @@ def run_b200(a, rank, world, dist):
                                                   for k, v in prof.items()},
         "render_stats": st0, "per_layer": sweep,
         **({"multiview": multiview} if multiview else {}),
+        **({"short_groups": short_groups} if short_groups else {}),
         # whole-frame HBM roofline: algorithmic bytes of one
         # decoded+rendered frame x fps against the HBM peak
         "frame_roofline": {"bytes_per_frame": int(frame_bytes),

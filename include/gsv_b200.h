@@ -106,6 +106,11 @@ int gsv_read_info(const uint8_t* data, size_t len, gsv_info* out);
 int gsv_read_group(const uint8_t* data, size_t len, int group, gsv_group_info* out);
 int gsv_read_entry(const uint8_t* data, size_t len, int group, int layer, int entry,
                    gsv_entry_info* out);
+/* the whole directory in one parse: groups[group_count] and every entry in
+ * (group, layer, entry) order; *n_entries gets the entry count (also when the
+ * buffers are too small, which fails with GSV_E_INVALID_INPUT). */
+int gsv_read_directory(const uint8_t* data, size_t len, gsv_group_info* groups, size_t group_cap,
+                       gsv_entry_info* entries, size_t entry_cap, size_t* n_entries);
 
 /* ---- decode (read_layers / decode_video, container.py:260-310,
  *      pipeline.py:350-359) --------------------------------------------------

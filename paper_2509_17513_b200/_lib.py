@@ -73,6 +73,7 @@ _SIGS = {
     "gsv_session_check_capacity": (_I, [_P]),
     "gsv_read_info": (_I, [_P, _SZ, ctypes.POINTER(Info_t)]),
     "gsv_read_group": (_I, [_P, _SZ, _I, ctypes.POINTER(GroupInfo_t)]),
+    "gsv_read_directory": (_I, [_P, _SZ, _P, _SZ, _P, _SZ, ctypes.POINTER(_SZ)]),
     "gsv_read_entry": (_I, [_P, _SZ, _I, _I, _I, ctypes.POINTER(EntryInfo_t)]),
     "gsv_video_open": (_I, [_P, _P, _SZ, _I, ctypes.POINTER(_P)]),
     "gsv_video_open_groups": (_I, [_P, _P, _SZ, _I, _I, _I, ctypes.POINTER(_P)]),

@@ -111,23 +111,30 @@ def _read_all(source) -> bytes:
 
 
 def _structure_from_bytes(data: bytes) -> ContainerInfo:
+    """read_structure from the container bytes: one native parse of the
+    whole directory (gsv_read_directory), the reference's checks and messages."""
     L = _lib.load()
     info = _lib.Info_t()
     check(L.gsv_read_info(data, len(data), ctypes.byref(info)))
-    groups = []
-    for g in range(info.group_count):
-        gi = _lib.GroupInfo_t()
-        check(L.gsv_read_group(data, len(data), g, ctypes.byref(gi)))
+    G = int(info.group_count)
+    gis = (_lib.GroupInfo_t * max(G, 1))()
+    n = ctypes.c_size_t(0)
+    L.gsv_read_directory(data, len(data), gis, G, None, 0, ctypes.byref(n))  # entry count
+    ents = (_lib.EntryInfo_t * max(int(n.value), 1))()
+    check(L.gsv_read_directory(data, len(data), gis, G, ents, int(n.value), ctypes.byref(n)))
+    groups, k = [], 0
+    for g in range(G):
+        gi = gis[g]
         layers = []
         for l in range(info.layer_count):
-            ents = []
-            for e in range(gi.channel_counts[l]):
-                ei = _lib.EntryInfo_t()
-                check(L.gsv_read_entry(data, len(data), g, l, e, ctypes.byref(ei)))
-                ents.append(ChannelEntry(ChannelId(ATTRIBUTE_NAMES[ei.attribute], ei.component),
-                                         ei.bits, ei.offset, ei.size, float(ei.range_min),
-                                         float(ei.range_max)))
-            layers.append(tuple(ents))
+            row = []
+            for _ in range(gi.channel_counts[l]):
+                ei = ents[k]
+                k += 1
+                row.append(ChannelEntry(ChannelId(ATTRIBUTE_NAMES[ei.attribute], ei.component),
+                                        ei.bits, ei.offset, ei.size, float(ei.range_min),
+                                        float(ei.range_max)))
+            layers.append(tuple(row))
         groups.append(GroupDirectory(gi.start_frame, gi.frame_count, gi.position_bits,
                                      tuple(gi.layer_counts[:info.layer_count]), tuple(layers)))
     return ContainerInfo(info.version, info.layer_count, info.sh_degree,
@@ -247,7 +254,8 @@ class DeviceVideo:
                 data, info, k = _read_prefix(f, up_to_layer)
         elif isinstance(source, (bytes, bytearray, memoryview)):
             data = bytes(source)
-            info = _structure_from_bytes(data)
+            if info is None:
+                info = _structure_from_bytes(data)
             k = info.layer_count if up_to_layer is None else up_to_layer
         else:
             data, info, k = _read_prefix(source, up_to_layer)

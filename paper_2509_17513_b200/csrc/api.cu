@@ -10,9 +10,11 @@
 // reference would), the GPU decodes and CRC-checks every run before that
 // point, and the earliest failure in the reference's order is reported.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
@@ -385,6 +387,15 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                int up_to_layer, gsv_video** out, int g0 = 0, int g1 = -1) {
     *out = nullptr;
     t_stage.reset();
+    static const bool dbg_t = getenv("GSV_DEBUG_OPEN_TIMING") != nullptr;  // dev: phase times to stderr
+    auto T = [&](const char* what) {
+        static thread_local std::chrono::steady_clock::time_point last;
+        const auto now = std::chrono::steady_clock::now();
+        if (dbg_t && what) fprintf(stderr, "[open] %s %.2f ms\n", what,
+                                   std::chrono::duration<double, std::milli>(now - last).count());
+        last = now;
+    };
+    T(nullptr);
     gsv_video* v = new gsv_video();
     v->s = s;
     auto bail = [&](int rc) {
@@ -448,6 +459,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
         return v->d_payload.as<uint8_t>() + dev_base[g] + (off - lo[g]);
     };
 
+    T("parse+stage");
     // ---- walk entries in the reference's order ----------------------------
     const int shdim_ok = c.sh_degree <= 3;
     const int shdim = shdim_ok ? 3 * (c.sh_degree + 1) * (c.sh_degree + 1) : 0;
@@ -519,8 +531,10 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
         }
     }
 
+    T("walk");
     // ---- decode + CRC on the GPU ------------------------------------------
     if ((rc = v->runs.decode(st))) return bail(rc);
+    T("decode+crc");
     ErrKey best = stop;
     if (pending.set() && (!best.set() || pending.order < best.order ||
                           (pending.order == best.order && pending.phase < best.phase)))
@@ -564,8 +578,10 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                 }
         }
     }
+    T("frame tables");
     if ((rc = upload(v->d_slots, sd, st))) return bail(rc);
     GSV_CUDA(cudaStreamSynchronize(st));
+    T("upload");
     *out = v;
     return GSV_OK;
 }

@@ -342,6 +342,43 @@ int gsv_read_entry(const uint8_t* data, size_t len, int group, int layer, int en
     return GSV_OK;
 }
 
+int gsv_read_directory(const uint8_t* data, size_t len, gsv_group_info* groups, size_t group_cap,
+                       gsv_entry_info* entries, size_t entry_cap, size_t* n_entries) {
+    Container c;
+    int rc = parse_container(data, len, &c);
+    if (rc) return rc;
+    if (c.layer_count > 64) return fail(GSV_E_INVALID_INPUT, "more than 64 layers");
+    size_t ne = 0;
+    for (const GroupDir& g : c.groups)
+        for (int l = 0; l < c.layer_count; l++) ne += g.channels[l].size();
+    if (n_entries) *n_entries = ne;
+    if (c.groups.size() > group_cap || ne > entry_cap) return fail(GSV_E_INVALID_INPUT, "directory buffers too small");
+    size_t k = 0;
+    for (size_t gi = 0; gi < c.groups.size(); gi++) {
+        const GroupDir& g = c.groups[gi];
+        gsv_group_info* o = groups + gi;
+        memset(o, 0, sizeof *o);
+        o->start_frame = g.start_frame;
+        o->frame_count = g.frame_count;
+        o->position_bits = g.position_bits;
+        for (int l = 0; l < c.layer_count; l++) {
+            o->layer_counts[l] = g.layer_counts[l];
+            o->channel_counts[l] = (uint32_t)g.channels[l].size();
+            for (const Entry& e : g.channels[l]) {
+                gsv_entry_info* q = entries + k++;
+                q->attribute = e.attr;
+                q->component = e.comp;
+                q->bits = e.bits;
+                q->offset = e.offset;
+                q->size = e.size;
+                q->range_min = e.rmin;
+                q->range_max = e.rmax;
+            }
+        }
+    }
+    return GSV_OK;
+}
+
 // _encode_reference_body (codec.py:137-163) -> body bytes (flag + modes + blocks),
 // or the whole-run raw fallback.  samples: count*h*w values < 2^bits.
 int64_t gsv_encode_reference_body(const uint32_t* samples, int count, int h, int w, int bits,
