@@ -820,6 +820,7 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
             }
         }
         for (int i = 0; i < nstreams; i++) {
+            if (int rc = readback_counters(s->aux_work[i], s->aux[i])) return rc;
             GSV_CUDA(cudaEventRecord(s->ev_join[i], s->aux[i]));
             GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join[i], 0));
             if (host_rgb8) {

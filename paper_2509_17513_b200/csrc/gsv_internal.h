@@ -232,6 +232,8 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
 // render.cu: full per-frame pipeline
 int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
                   uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
+// counters of w to its pinned mirror on s (after an enqueue-only batch)
+int readback_counters(RenderWork* w, cudaStream_t s);
 int render_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,
                uint8_t* out_rgb8, gsv_render_stats* stats, cudaStream_t s);
 int render_splats2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, float* out_rgb,

@@ -543,7 +543,7 @@ static unsigned debug_skip() {
 // Enqueue one frame.  `project` enqueues the projection kernel into w.
 template <class Proj>
 static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj project,
-                          float* out_rgb, uint8_t* out_rgb8, cudaStream_t s) {
+                          float* out_rgb, uint8_t* out_rgb8, cudaStream_t s, bool readback = true) {
     const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
     const int ntiles = ntx * nty;
     const int64_t npix = (int64_t)cam.width * cam.height;
@@ -605,8 +605,16 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         count_launch(1);
     }
     prof_mark(ST_COUNT, s);
-    cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    // counters to the pinned mirror (a frame-parallel batch reads them back
+    // once per stream at its end instead: the key-capacity maximum is sticky)
+    if (readback) cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     GSV_CUDA(cudaGetLastError());
+    return GSV_OK;
+}
+
+int readback_counters(RenderWork* w, cudaStream_t s) {
+    if (!w->ctr) return GSV_OK;
+    GSV_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     return GSV_OK;
 }
 
@@ -641,7 +649,7 @@ int render_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, float* 
     const int64_t n = src.layer_off[src.nlayers];
     auto proj = [&]() { launch_project_planes(src, cam, w, s); };
     if (stats == reinterpret_cast<gsv_render_stats*>(1)) {  // enqueue only (throughput mode)
-        return render_enqueue(n, cam, w, proj, out_rgb, out_rgb8, s);
+        return render_enqueue(n, cam, w, proj, out_rgb, out_rgb8, s, false);
     }
     return render_checked(n, cam, w, proj, out_rgb, out_rgb8, stats, s);
 }
