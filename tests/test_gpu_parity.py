@@ -307,3 +307,33 @@ def test_open_group_range(gsvb):
         start += info.groups[g].frame_count
     with pytest.raises(gsvb.InvalidInputError):
         gsvb.DeviceVideo(data, k, groups=(G, G + 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["huge_splats", "tiny_image", "behind_camera", "many_rounds"])
+def test_render_edge_cases(gsvb, case):
+    """Edge cases of the tiled compositor against the oracle: splats that
+    cover the whole image (key buffers grow and re-render), an image smaller
+    than one tile (partial tiles on both axes), every splat culled (pure
+    background), and more splats than the first depth-rank round holds (open
+    tiles carried into a second round)."""
+    from paper_2509_17513_b200.synth import SceneSpec, iter_frames
+    from paper_2509_17513_b200.types import Camera
+    if case == "huge_splats":
+        spec, W, H, eye = SceneSpec(count=2000, frames=1, sh_degree=1, scale_range=(0.3, 0.9)), 160, 120, (0, 0, -2.5)
+    elif case == "tiny_image":
+        spec, W, H, eye = SceneSpec(count=500, frames=1, sh_degree=2, scale_range=(0.02, 0.1)), 13, 9, (0.4, 0.2, -2.4)
+    elif case == "behind_camera":
+        spec, W, H, eye = SceneSpec(count=500, frames=1, sh_degree=0, scale_range=(0.02, 0.1)), 64, 48, (0, 0, 5.0)
+    else:
+        spec, W, H, eye = SceneSpec(count=40_000, frames=1, sh_degree=1, scale_range=(0.004, 0.03)), 320, 240, (0.3, -0.2, -2.5)
+    g = next(iter(iter_frames(spec, 777)))
+    cam = Camera.looking_at(eye=eye, target=(0, 0, 0.0 if case != "behind_camera" else 10.0),
+                            fov_deg=60.0, width=W, height=H, near=0.01,
+                            background=(0.2, 0.1, 0.05))
+    img = gsvb.render_set(g, cam).pixels
+    ref = O.render_set(g, cam)
+    assert img.shape == (H, W, 3)
+    assert np.max(np.abs(img - ref)) <= MAX_ABS, case
+    if case == "behind_camera":
+        assert np.array_equal(img, np.tile(np.asarray(cam.background, np.float64), (H, W, 1)).astype(np.float32))
