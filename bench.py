@@ -296,6 +296,7 @@ def run_b200(a, rank, world, dist):
         step_resident(codec, a.layers, verify=True).close()
 
     host_ms = [0.0]
+    local_ms = [0.0]
 
     def timed(codec, k, steps, warmup, e2e=False):
         pinned = None
@@ -337,6 +338,7 @@ def run_b200(a, rank, world, dist):
         # window because the events bracket every call on the same stream
         host_ms[0] = t_enq * 1e3 / steps
         ms = max(ms, t_host * 1e3)
+        local_ms[0] = ms
         torch.cuda.synchronize()
         if dist:
             tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -348,6 +350,16 @@ def run_b200(a, rank, world, dist):
     with Clocks(dev) as clk:
         fps, ms_step, launches = timed(a.codec, a.k, a.steps, a.warmup)
     clocks = clk.summary()
+    # per-rank metrics gathered to rank 0 over NCCL (after the timed region):
+    # each rank's own step time and a checksum of its last rendered frame
+    ranks = None
+    if dist:
+        mine = torch.tensor([float(rank), local_ms[0] / a.steps, float(outs[-1].double().sum())],
+                            dtype=torch.float64, device="cuda")
+        got = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(got, mine)
+        ranks = [{"rank": int(x[0].item()), "ms_per_step": round(x[1].item(), 3),
+                  "last_frame_sum": round(x[2].item(), 3)} for x in got]
     host_ms_step = host_ms[0]
 
     # stage profile of one step (separate pass: events perturb timing slightly)
@@ -410,6 +422,7 @@ def run_b200(a, rank, world, dist):
         "roofline": roof, "stages_ms_per_frame": {k: round(v["ms"] / a.frames, 5)
                                                   for k, v in prof.items()},
         "render_stats": st0, "per_layer": sweep,
+        **({"ranks": ranks} if ranks else {}),
         **({"multiview": multiview} if multiview else {}),
         **({"short_groups": short_groups} if short_groups else {}),
         # whole-frame HBM roofline: algorithmic bytes of one
