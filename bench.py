@@ -263,7 +263,7 @@ def run_b200(a, rank, world, dist):
     import paper_2509_17513_b200 as gsvb
     from paper_2509_17513_b200 import _lib
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     blobs, key = make_inputs(a, 1002 + rank)
     cam = camera(a)
@@ -643,8 +643,11 @@ def main():
         import torch
         import torch.distributed as td
         backend = "nccl" if a.impl == "b200" and torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        # GSV_BENCH_BACKEND=gloo: dev check of the multi-rank path with ranks
+        # sharing one GPU (NCCL needs one GPU per rank)
+        backend = os.environ.get("GSV_BENCH_BACKEND", backend)
+        if a.impl == "b200" and torch.cuda.is_available():
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
         td.init_process_group(backend=backend)
         dist = td
     if a.impl == "reference":
