@@ -517,6 +517,9 @@ static unsigned debug_double() {  // GSV_DEBUG_DOUBLE: stages launched twice (ma
             if (strstr(e, "dsort")) mask |= 4;
             if (strstr(e, "emit")) mask |= 8;
             if (strstr(e, "project")) mask |= 16;
+            if (strstr(e, "gather")) mask |= 32;
+            if (strstr(e, "fixup")) mask |= 64;
+            if (strstr(e, "lastround")) mask |= 128;
         }
         init = 1;
     }
@@ -558,7 +561,12 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                                           ntiles, open_word(composite_rows()));
     const unsigned skip = debug_skip(), dbl = debug_double();
     if (!(skip & 16)) project();
-    if (dbl & 16) project();
+    if (dbl & 16) {  // the second projection counts into spare counter slots
+        unsigned long long* keep = w->ctr;
+        w->ctr = keep + 12;
+        project();
+        w->ctr = keep;
+    }
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
@@ -566,11 +574,14 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         if (!(skip & 4)) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         if (dbl & 4) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
+        if (dbl & 64)
+            depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         count_launch(2 + radix_launches(4, true));
     }
     prof_mark(ST_EMIT, s);
     const unsigned g = 148 * 4;
     gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
+    if (dbl & 32) gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
     count_launch(1);
     std::vector<uint32_t> bounds;
     round_bounds(n, &bounds);
@@ -602,6 +613,9 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         if (!(skip & 1))
             launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
                                    w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
+        if ((dbl & 128) && j > 0 && j + 2 == bounds.size())
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+                                   w->tile_done, cam, false, true, out_rgb, out_rgb8, s);
         count_launch(1);
     }
     prof_mark(ST_COUNT, s);
