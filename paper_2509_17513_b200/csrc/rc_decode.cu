@@ -14,7 +14,11 @@
 //     a 4-word register queue of aligned loads issued ~16 bytes ahead, and
 //     the (at most two) renormalisation shifts per decision are branch-free;
 //   * residual reconstruction works a 32-bit word (4/NB samples) at a time,
-//     reading the previous plane and writing the output as aligned words.
+//     reading the previous plane and writing the output as aligned words;
+//   * (variant 3, the default) a byte whose leading M decisions all take the
+//     zero branch is recognised with M multiplies and one compare instead of
+//     M full decisions: the high byte of 16-bit position residuals (M = 8)
+//     and the top nibble of 8-bit residuals (M = 4), exact fallback otherwise.
 // RAW-mode planes of these runs are first copied to 16-B aligned storage so
 // that every predictor plane is aligned.
 #include <stdint.h>
@@ -330,10 +334,171 @@ __device__ __forceinline__ uint32_t decode_byte_v2(uint32_t T, uint32_t Tn, uint
     return ctx & 0xFFu;
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Variant 3: zero-prefix test.  Along the all-zero path of a bit tree
+// (nodes 1, 2, 4, ..., 2^(M-1)) a 0 decision leaves `code` alone and sets
+// rng = bound, so the nested intervals [0, bound_k) shrink and the first M
+// decisions are all 0 iff the code (shifted by the renormalisation bytes
+// taken before decision M-1, which preserves the order of code and bound)
+// lies below the last bound.  That bound chain needs only rng and the M
+// zero-path probabilities, not the bits, so M decisions cost M multiplies
+// and one compare.  Position residuals (2-byte samples) have a zero high
+// byte (M = 8: the whole byte) and 1-byte residuals are small (M = 4); when
+// the test fails the byte is decoded by variant 2 from the untouched state.
+template <int M, bool SAME_TREE>
+__device__ __forceinline__ uint32_t decode_byte_v3(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
+                                                   uint32_t& code, CodedStream& cs) {
+    static_assert(M >= 2 && M <= 8, "zero prefix length");
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t z[M + 1];  // zero-path probabilities (z[M]: the node decision M starts at)
+    z[0] = q0.y;
+    z[1] = q0.z;
+#pragma unroll
+    for (int k = 2; k <= M && k < 8; k++) z[k] = lds_u32(T + 4u * (1u << k));
+    uint4 qn = q0, cq = make_uint4(0u, 0u, 0u, 0u), nq0 = cq;
+    if (!SAME_TREE) qn = lds_quad(Tn);
+    if (M < 8) cq = lds_quad(T + 16u * (1u << (M - 1)));  // children of node 2^M
+    if (M < 6) nq0 = lds_quad(T + 16u * (1u << M));       // its grandchildren
+    uint32_t a = rng >> 12, rmin = 0xFFFFFFFFu, S = 0, bound = 0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+        bound = a * z[k];
+        rmin = min(rmin, bound);
+        const bool lt24 = bound < (1u << 24);
+        a = lt24 ? shr_opaque<4>(bound) : shr_opaque<12>(bound);
+        if (k < M - 1) S += lt24 ? 1u : 0u;
+    }
+    // (code:bhi) << 8S must stay below bound as a 64-bit value: no code
+    // bits may be shifted out (the zero path would have failed earlier)
+    if (__funnelshift_lc(code, 0u, 8u * S) != 0u || !(__funnelshift_lc(bhi, code, 8u * S) < bound) ||
+        rmin < (1u << 16) || S > 3u)
+        return decode_byte_v2<SAME_TREE>(T, Tn, q0, rng, code, cs);
+    const uint32_t rng0 = rng, code0 = code;
+    const bool lt24 = bound < (1u << 24);
+    S += lt24 ? 1u : 0u;
+    rng = lt24 ? bound << 8 : bound;
+    code = __funnelshift_lc(bhi, code, 8u * S);
+    uint32_t pn[8], na[8];
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+        pn[k] = z[k] + ((4096u - z[k]) >> 4);
+        na[k] = T + 4u * (1u << k);
+    }
+    uint32_t sel = 0x2107u - S;
+    uint32_t node = T + 4u * (1u << (M < 8 ? M : 0));
+    if (M < 8) {
+        uint32_t p = z[M < 8 ? M : 0];
+        const uint32_t m3T = 0u - 3u * T, c0T = 0u - T, c1T = 4u - T;
+        uint32_t pbit = 0u;
+#pragma unroll
+        for (int k = M; k < 8; k++) {
+            uint4 nq = make_uint4(0u, 0u, 0u, 0u);
+            if (k == M) nq = nq0;
+            else if (k < 6) nq = lds_quad(4u * node + m3T);
+            na[k] = node;
+            const uint32_t c0 = pbit ? cq.z : cq.x;
+            const uint32_t c1 = pbit ? cq.w : cq.y;
+            uint32_t bitv, nnode;
+            asm("{\n\t"
+                ".reg .pred pb, pl;\n\t"
+                ".reg .u32 bnd, r1, r, t4, t12, K, d, off;\n\t"
+                "mul.lo.u32 bnd, %0, %9;\n\t"
+                "setp.ge.u32 pb, %2, bnd;\n\t"
+                "sub.u32 r1, %1, bnd;\n\t"
+                "selp.u32 r, r1, bnd, pb;\n\t"
+                "@pb sub.u32 %2, %2, bnd;\n\t"
+                "setp.lt.u32 pl, r, 16777216;\n\t"
+                "min.u32 %4, %4, r;\n\t"
+                "shr.u32 t4, r, 4;\n\t"
+                "shr.u32 t12, r, 12;\n\t"
+                "selp.u32 %0, t4, t12, pl;\n\t"
+                "@pl shl.b32 r, r, 8;\n\t"
+                "@pl prmt.b32 %2, %2, %10, %3;\n\t"
+                "@pl sub.u32 %3, %3, 1;\n\t"
+                "mov.u32 %1, r;\n\t"
+                "selp.u32 K, 15, 4096, pb;\n\t"
+                "sub.s32 d, K, %9;\n\t"
+                "shr.s32 d, d, 4;\n\t"
+                "add.u32 %5, %9, d;\n\t"
+                "selp.u32 %6, %12, %11, pb;\n\t"
+                "selp.u32 off, %14, %13, pb;\n\t"
+                "mad.lo.u32 %7, %15, 2, off;\n\t"
+                "selp.u32 %8, 1, 0, pb;\n\t"
+                "}"
+                : "+r"(a), "+r"(rng), "+r"(code), "+r"(sel), "+r"(rmin), "=r"(pn[k]), "=r"(p), "=r"(nnode),
+                  "=r"(bitv)
+                : "r"(p), "r"(bhi), "r"(c0), "r"(c1), "r"(c0T), "r"(c1T), "r"(node));
+            node = nnode;
+            pbit = bitv;
+            cq = nq;
+        }
+        if (rmin < (1u << 16) || 0x2107u - sel > 4u) {
+            rng = rng0;
+            code = code0;
+            return decode_byte_slow(T, Tn, q0, rng, code, cs);
+        }
+    }
+    const uint32_t used = 0x2107u - sel;
+#pragma unroll
+    for (int k = 0; k < 8; k++) sts_u32(na[k], pn[k]);
+    const uint32_t ctx = M < 8 ? (node - T) >> 2 : 256u;
+    if (SAME_TREE) {  // first decision was 0: nodes 1 and 2 were updated
+        qn.y = pn[0];
+        qn.z = pn[1];
+    }
+    q0 = qn;
+    cs.bb <<= 8 * used;
+    cs.nbits -= (int32_t)(8 * used);
+    cs.refill();
+    return ctx & 0xFFu;
+}
+
+// Whole-byte zero test (M = 8, next tree Tn != T): true and the state
+// advanced past a zero byte, or false and nothing touched (the caller then
+// decodes the byte with its single variant-2 instance).
+__device__ __forceinline__ bool zero_byte(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng, uint32_t& code,
+                                          CodedStream& cs) {
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t z[8];
+    z[0] = q0.y;
+    z[1] = q0.z;
+#pragma unroll
+    for (int k = 2; k < 8; k++) z[k] = lds_u32(T + 4u * (1u << k));
+    uint32_t a = rng >> 12, rmin = 0xFFFFFFFFu, S = 0, bound = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        bound = a * z[k];
+        rmin = min(rmin, bound);
+        const bool lt24 = bound < (1u << 24);
+        a = lt24 ? shr_opaque<4>(bound) : shr_opaque<12>(bound);
+        if (k < 7) S += lt24 ? 1u : 0u;
+    }
+    if (__funnelshift_lc(code, 0u, 8u * S) != 0u || !(__funnelshift_lc(bhi, code, 8u * S) < bound) ||
+        rmin < (1u << 16) || S > 3u)
+        return false;
+    const uint4 qn = lds_quad(Tn);
+    const bool lt24 = bound < (1u << 24);
+    S += lt24 ? 1u : 0u;
+    rng = lt24 ? bound << 8 : bound;
+    code = __funnelshift_lc(bhi, code, 8u * S);
+#pragma unroll
+    for (int k = 0; k < 8; k++) sts_u32(T + 4u * (1u << k), z[k] + ((4096u - z[k]) >> 4));
+    q0 = qn;
+    cs.bb <<= 8 * S;
+    cs.nbits -= (int32_t)(8 * S);
+    cs.refill();
+    return true;
+}
+
 template <int V, bool SAME_TREE>
 __device__ __forceinline__ uint32_t decode_byte_v(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
                                                   uint32_t& code, CodedStream& cs) {
-    if constexpr (V == 2) return decode_byte_v2<SAME_TREE>(T, Tn, q0, rng, code, cs);
+    if constexpr (V >= 2) return decode_byte_v2<SAME_TREE>(T, Tn, q0, rng, code, cs);
     else return decode_byte<SAME_TREE>(T, Tn, q0, rng, code, cs);
 }
 
@@ -368,14 +533,25 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
             uint32_t ow = 0, z = 0;
             // one byte per iteration and a single inlined decoder instance,
             // so the loop body stays small in the instruction cache
+            // (variant 3, 2-byte samples: one sample per iteration, the high
+            // byte by the zero test with a cold variant-2 fallback)
+            constexpr int BPI = (V == 3 && NB == 2) ? 2 : 1;
 #pragma unroll 1
-            for (int e = 0; e < SPW * NB; e++) {
+            for (int e = 0; e < SPW * NB; e += BPI) {
                 const int j = e / NB, b = e % NB;
                 if (SPW > 1 && idx >= hw) break;
                 const uint32_t T = P + (uint32_t)b * kTreeBytes;
                 const uint32_t Tn = NB == 1 ? T : P + (uint32_t)((b + 1) % NB) * kTreeBytes;
-                z |= decode_byte_v<V, NB == 1>(T, Tn, q0, rng, code, cs) << (8 * b);
-                if (b == NB - 1) {
+                if (V == 3 && NB == 2) {
+                    const uint32_t T1 = P + kTreeBytes;
+                    z = decode_byte_v2<false>(P, T1, q0, rng, code, cs);
+                    if (!zero_byte(T1, P, q0, rng, code, cs)) z |= decode_byte_v2<false>(T1, P, q0, rng, code, cs) << 8;
+                } else if (V == 3 && NB == 1) {
+                    z = decode_byte_v3<4, true>(T, Tn, q0, rng, code, cs);
+                } else {
+                    z |= decode_byte_v<V, NB == 1>(T, Tn, q0, rng, code, cs) << (8 * b);
+                }
+                if (b + BPI - 1 == NB - 1) {
                     uint32_t pred;
                     if (PREV) {
                         pred = (pw >> (8 * NB * j)) & mask;
@@ -461,8 +637,11 @@ void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n
     if (c.blk[3] == 0) return;
     const size_t smem = (size_t)lane_stride(nbmax) * kRPW;
     const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
-    const int v = ev ? atoi(ev) : 2;
-    if (v == 1) {
+    const int v = ev ? atoi(ev) : 3;
+    if (v == 3) {
+        cudaFuncSetAttribute(rc_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rc_decode_kernel<3><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+    } else if (v == 1) {
         cudaFuncSetAttribute(rc_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         rc_decode_kernel<1><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
     } else {
