@@ -204,6 +204,42 @@ int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* po
 int gsv_decode_payload_host(gsv_session* s, const uint8_t* blob, size_t len,
                             uint32_t* samples, size_t capacity, int32_t* hdr);
 
+/* ---- encoder: GPU quantisation + codec-1 range coding --
+ * gsv_quantize_channels: quantize_channel (quantize.py:79-106, f32 range
+ * cover quantize.py:62-76) of nch channels of one group, each channel a
+ * (frames, n) block of fp64 values on the device (value (f, j) at
+ * values[f * frame_stride + j]), written as frames padded planes
+ * (flatten_to_plane, quantize.py:160-167) of width*height LE samples at
+ * `planes` (device); range_min / range_max receive the stored f32 range.
+ * Non-finite input -> GSV_E_INVALID_INPUT "non-finite channel values".
+ * Synchronises the session stream. */
+typedef struct gsv_quant_channel {
+    const double* values;       /* device */
+    uint8_t* planes;            /* device: frames * width * height * bits/8 bytes */
+    uint64_t frame_stride;      /* elements between frames (>= n) */
+    uint32_t frames, n, width, height, bits;
+    float range_min, range_max; /* out */
+} gsv_quant_channel;
+int gsv_quantize_channels(gsv_session* s, gsv_quant_channel* ch, int nch);
+
+/* gsv_encode_runs: for every run, the codec-1 payload body of
+ * _encode_reference_body (codec.py:137-163: per-plane range coding through
+ * encode_bittree, _rc.py:55-118, RAW planes where coding does not pay, the
+ * whole-run raw fallback) into `body` (device, gsv_encode_body_capacity
+ * bytes), and the payload CRC-32 of the samples (encode_planes,
+ * codec.py:166-180).  body_len / checksum are written back; the payload is
+ * header `<BBHHHHI` + body[0:body_len] + checksum.  Synchronises. */
+typedef struct gsv_encode_run {
+    const uint8_t* samples; /* device: count * width * height LE samples */
+    uint8_t* body;          /* device */
+    uint32_t count, width, height, bits;
+    uint64_t body_len;      /* out */
+    uint32_t checksum;      /* out */
+    uint32_t reserved;
+} gsv_encode_run;
+uint64_t gsv_encode_body_capacity(uint32_t count, uint32_t width, uint32_t height, uint32_t bits);
+int gsv_encode_runs(gsv_session* s, gsv_encode_run* runs, int nruns);
+
 /* ---- instrumentation ------------------------------------------------------
  * gsv_kernel_launches: kernels launched by this library so far (process-wide).
  * gsv_profile_enable(1) resets and starts stage timing with CUDA events on the

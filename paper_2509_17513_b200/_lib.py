@@ -58,6 +58,19 @@ class RenderStats_t(ctypes.Structure):
                 ("n_keys_emitted", ctypes.c_int64)]
 
 
+class QuantChannel_t(ctypes.Structure):
+    _fields_ = [("values", ctypes.c_void_p), ("planes", ctypes.c_void_p), ("frame_stride", ctypes.c_uint64),
+                ("frames", ctypes.c_uint32), ("n", ctypes.c_uint32), ("width", ctypes.c_uint32),
+                ("height", ctypes.c_uint32), ("bits", ctypes.c_uint32), ("range_min", ctypes.c_float),
+                ("range_max", ctypes.c_float)]
+
+
+class EncodeRun_t(ctypes.Structure):
+    _fields_ = [("samples", ctypes.c_void_p), ("body", ctypes.c_void_p), ("count", ctypes.c_uint32),
+                ("width", ctypes.c_uint32), ("height", ctypes.c_uint32), ("bits", ctypes.c_uint32),
+                ("body_len", ctypes.c_uint64), ("checksum", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _I64 = ctypes.c_int64
@@ -97,6 +110,9 @@ _SIGS = {
                                _P, _P, ctypes.POINTER(_I64)]),
     "gsv_decode_payload_host": (_I, [_P, _P, _SZ, _P, _SZ, _P]),
     "gsv_encode_reference_body": (_I64, [_P, _I, _I, _I, _I, _P, _SZ]),
+    "gsv_quantize_channels": (_I, [_P, _P, _I]),
+    "gsv_encode_body_capacity": (ctypes.c_uint64, [ctypes.c_uint32] * 4),
+    "gsv_encode_runs": (_I, [_P, _P, _I]),
     "gsv_crc32": (ctypes.c_uint32, [_P, _SZ]),
     "gsv_kernel_launches": (ctypes.c_longlong, []),
     "gsv_profile_enable": (_I, [_I]),

@@ -26,6 +26,7 @@ SOURCES = {
     "container.cpp": [],
     "decode.cu": ["-fmad=false"],
     "rc_decode.cu": [],
+    "encode.cu": ["-fmad=false"],
     "project.cu": ["-fmad=false"],
     "sort.cu": [],
     "composite.cu": [],

@@ -924,6 +924,142 @@ int gsv_fold_deltas(gsv_session* s, int64_t n, int shdim, double* pos, double* r
     return GSV_OK;
 }
 
+// ---- encoder ---------------------------------------------
+int gsv_quantize_channels(gsv_session* s, gsv_quant_channel* ch, int nch) {
+    if (nch < 0 || (nch > 0 && !ch)) return fail(GSV_E_INVALID_INPUT, "invalid channel list");
+    if (nch == 0) return GSV_OK;
+    std::vector<QuantChannel> qc(nch);
+    uint64_t max_values = 0, max_samples = 0;
+    for (int i = 0; i < nch; i++) {
+        const gsv_quant_channel& c = ch[i];
+        if (c.bits != 8 && c.bits != 16 && c.bits != 32) return fail(GSV_E_INVALID_INPUT, "bits must be one of (8, 16, 32)");
+        if (c.frames == 0 || c.n == 0) return fail(GSV_E_INVALID_INPUT, "empty channel");
+        if ((uint64_t)c.width * c.height < c.n) return fail(GSV_E_INVALID_INPUT, "plane smaller than the channel");
+        if (c.frame_stride < c.n) return fail(GSV_E_INVALID_INPUT, "frame stride smaller than the channel");
+        qc[i] = QuantChannel{c.values, c.planes, c.frame_stride, c.frames, c.n, c.width, c.height, c.bits};
+        max_values = std::max<uint64_t>(max_values, (uint64_t)c.frames * c.n);
+        max_samples = std::max<uint64_t>(max_samples, (uint64_t)c.frames * c.width * c.height);
+    }
+    cudaStream_t st = s->stream;
+    DevBuf d_ch, d_red, d_rng;
+    int rc = upload(d_ch, qc, st);
+    if (rc) return rc;
+    if ((rc = d_red.alloc((size_t)nch * 3 * 8))) return rc;
+    if ((rc = d_rng.alloc((size_t)nch * 2 * 4))) return rc;
+    std::vector<unsigned long long> init((size_t)nch * 3);
+    for (int i = 0; i < nch; i++) {
+        init[3 * i] = ~0ull;
+        init[3 * i + 1] = 0ull;
+        init[3 * i + 2] = 0ull;
+    }
+    GSV_CUDA(cudaMemcpyAsync(d_red.p, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st));
+    launch_quantize(d_ch.as<QuantChannel>(), nch, max_values, max_samples, d_red.as<unsigned long long>(),
+                    d_rng.as<float>(), st);
+    count_launch(3);
+    std::vector<unsigned long long> red((size_t)nch * 3);
+    std::vector<float> rng((size_t)nch * 2);
+    GSV_CUDA(cudaMemcpyAsync(red.data(), d_red.p, red.size() * 8, cudaMemcpyDeviceToHost, st));
+    GSV_CUDA(cudaMemcpyAsync(rng.data(), d_rng.p, rng.size() * 4, cudaMemcpyDeviceToHost, st));
+    GSV_CUDA(cudaStreamSynchronize(st));
+    GSV_CUDA(cudaGetLastError());
+    for (int i = 0; i < nch; i++) {
+        if (red[3 * i + 2]) return fail(GSV_E_INVALID_INPUT, "non-finite channel values");
+        ch[i].range_min = rng[2 * i];
+        ch[i].range_max = rng[2 * i + 1];
+    }
+    return GSV_OK;
+}
+
+uint64_t gsv_encode_body_capacity(uint32_t count, uint32_t width, uint32_t height, uint32_t bits) {
+    const uint64_t plane = (uint64_t)width * height * (bits / 8);
+    return plane * count + plane + count + 64;
+}
+
+int gsv_encode_runs(gsv_session* s, gsv_encode_run* runs, int nruns) {
+    if (nruns < 0 || (nruns > 0 && !runs)) return fail(GSV_E_INVALID_INPUT, "invalid run list");
+    if (nruns == 0) return GSV_OK;
+    cudaStream_t st = s->stream;
+    uint64_t nplan = 0, nchunks = 0;
+    std::vector<uint32_t> by_class[3];
+    for (int i = 0; i < nruns; i++) {
+        const gsv_encode_run& r = runs[i];
+        if (r.bits != 8 && r.bits != 16 && r.bits != 32) return fail(GSV_E_INVALID_INPUT, "bits must be one of (8, 16, 32)");
+        if (r.count == 0 || r.width == 0 || r.height == 0 || r.count > 0xFFFF || r.width > 0xFFFF || r.height > 0xFFFF)
+            return fail(GSV_E_INVALID_INPUT, "plane run exceeds u16 geometry limits");
+        nplan += r.count;
+        by_class[r.bits == 8 ? 0 : (r.bits == 16 ? 1 : 2)].push_back((uint32_t)i);
+    }
+    DevBuf d_snap, d_off, d_runs, d_order, d_res, d_prefix, d_rd, d_pl, d_chunk, d_crc;
+    size_t snap_words = 0;
+    for (int i = 0; i < nruns; i++) snap_words += 256u * (runs[i].bits / 8);
+    int rc;
+    if ((rc = d_snap.alloc(snap_words * 4))) return rc;
+    if ((rc = d_off.alloc(nplan * 8))) return rc;
+    std::vector<EncRun> er(nruns);
+    std::vector<RunDesc> rd(nruns);
+    std::vector<PlaneRef> pl;
+    std::vector<uint32_t> plane_prefix(nruns + 1, 0), chunk_prefix;
+    pl.reserve(nplan);
+    chunk_prefix.reserve(nplan + 1);
+    chunk_prefix.push_back(0);
+    size_t so = 0, po = 0;
+    for (int i = 0; i < nruns; i++) {
+        const gsv_encode_run& r = runs[i];
+        const uint32_t pb = r.width * r.height * (r.bits / 8);
+        er[i] = EncRun{r.samples, r.body, d_off.as<uint64_t>() + po, d_snap.as<uint32_t>() + so,
+                       r.count, r.width, r.height, r.bits};
+        so += 256u * (r.bits / 8);
+        po += r.count;
+        plane_prefix[i + 1] = plane_prefix[i] + r.count;
+        RunDesc d{};
+        d.plane_bytes = pb;
+        d.plane_base = (uint32_t)pl.size();
+        d.w = (uint16_t)r.width;
+        d.h = (uint16_t)r.height;
+        d.count = (uint16_t)r.count;
+        d.bits = (uint8_t)r.bits;
+        rd[i] = d;
+        for (uint32_t f = 0; f < r.count; f++) {
+            PlaneRef p{};
+            p.samples = r.samples + (size_t)f * pb;
+            p.run = (uint32_t)i;
+            p.f = f;
+            pl.push_back(p);
+            nchunks += (pb + 1023) / 1024;
+            chunk_prefix.push_back((uint32_t)nchunks);
+        }
+    }
+    std::vector<uint32_t> order;
+    for (auto& c : by_class) order.insert(order.end(), c.begin(), c.end());
+    const int n_cls[3] = {(int)by_class[0].size(), (int)by_class[1].size(), (int)by_class[2].size()};
+    if ((rc = upload(d_runs, er, st))) return rc;
+    if ((rc = upload(d_order, order, st))) return rc;
+    if ((rc = upload(d_prefix, plane_prefix, st))) return rc;
+    if ((rc = upload(d_rd, rd, st))) return rc;
+    if ((rc = upload(d_pl, pl, st))) return rc;
+    if ((rc = upload(d_chunk, chunk_prefix, st))) return rc;
+    if ((rc = d_res.alloc((size_t)nruns * sizeof(EncResult)))) return rc;
+    if ((rc = d_crc.alloc((size_t)nruns * 4))) return rc;
+    GSV_CUDA(cudaMemsetAsync(d_crc.p, 0, (size_t)nruns * 4, st));
+    launch_rc_encode(d_runs.as<EncRun>(), d_order.as<uint32_t>(), n_cls, d_res.as<EncResult>(),
+                     d_prefix.as<uint32_t>(), nruns, (uint32_t)nplan, st);
+    count_launch(2);
+    launch_crc(d_rd.as<RunDesc>(), d_pl.as<PlaneRef>(), (int)pl.size(), d_chunk.as<uint32_t>(),
+               (uint32_t)nchunks, d_crc.as<uint32_t>(), st);
+    if (nchunks) count_launch();
+    std::vector<EncResult> res(nruns);
+    std::vector<uint32_t> crc(nruns);
+    GSV_CUDA(cudaMemcpyAsync(res.data(), d_res.p, res.size() * sizeof(EncResult), cudaMemcpyDeviceToHost, st));
+    GSV_CUDA(cudaMemcpyAsync(crc.data(), d_crc.p, crc.size() * 4, cudaMemcpyDeviceToHost, st));
+    GSV_CUDA(cudaStreamSynchronize(st));
+    GSV_CUDA(cudaGetLastError());
+    for (int i = 0; i < nruns; i++) {
+        runs[i].body_len = res[i].body_len;
+        runs[i].checksum = crc[i];
+    }
+    return GSV_OK;
+}
+
 int gsv_decode_payload_host(gsv_session* s, const uint8_t* blob, size_t len, uint32_t* samples,
                             size_t capacity, int32_t* hdr) {
     if (len >= 14) {

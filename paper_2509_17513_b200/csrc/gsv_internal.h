@@ -198,6 +198,39 @@ struct RenderWork {
 int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix);
 void work_free(RenderWork* w);
 
+// ---- encoder (encode.cu) ----
+// one channel of one group: (frames, n) fp64 values -> padded w*h planes
+struct QuantChannel {
+    const double* values;   // value (f, j) at values[f * frame_stride + j]
+    uint8_t* planes;
+    uint64_t frame_stride;
+    uint32_t frames, n, w, h, bits;
+};
+// one run to range-code: count planes of w*h LE samples
+struct EncRun {
+    const uint8_t* samples;
+    uint8_t* body;       // payload body buffer (capacity per gsv_encode_body_capacity)
+    uint64_t* blk_off;   // per plane: offset of its block in the body
+    uint32_t* snap;      // NB*256 words: model snapshot
+    uint32_t count, w, h, bits;
+};
+struct EncResult {
+    uint64_t body_len;
+    uint32_t whole_raw;
+    uint32_t pad;
+};
+struct EncClasses {
+    int n[3];
+    int off[3];
+    int blk[4];
+    int lanes;  // runs per warp
+};
+void launch_quantize(const QuantChannel* d_ch, int nch, uint64_t max_values, uint64_t max_samples,
+                     unsigned long long* d_red, float* d_ranges, cudaStream_t s);
+void launch_rc_encode(const EncRun* d_runs, const uint32_t* d_order, const int* n_per_class,
+                      EncResult* d_res, const uint32_t* d_plane_prefix, int nruns, uint32_t nplanes,
+                      cudaStream_t s);
+
 // byte copy job (RAW planes of range-coded runs -> aligned storage)
 struct CopyJob {
     const uint8_t* src;

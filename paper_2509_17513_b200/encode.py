@@ -205,6 +205,132 @@ def _encode_group(frames: list, start: int, cfg: EncodeConfig, position_bits: in
     return _Group(start, len(frames), position_bits, sizes, layers)
 
 
+class _PendingGroup:
+    """A group quantised on the device, waiting for the batched range coder."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def _gpu_quantize_group(frames: list, start: int, cfg: EncodeConfig, position_bits: int, sess):
+    """_encode_group on the GPU, first half: the keyframe
+    ordering (prune, significance rank, layer sizes) stays on the host; the
+    frames are gathered into that order on the device, rotations
+    hemisphere-aligned (pipeline.py:200-207: flip = sign(((p0 + p1) + p2) +
+    p3), numpy's summation order), and every (layer, channel) is quantised
+    into padded planes by gsv_quantize_channels (encode.cu)."""
+    import torch
+
+    from . import _lib
+    L = _lib.load()
+    key = frames[0]
+    keep = _keep_after_prune(key.opacities, cfg.prune_fraction)
+    idx = keep[_significance_rank(key.take(keep), cfg.volume_weight)]
+    sizes = _layer_sizes(len(idx), cfg.fractions())
+    if any(s < 1 for s in sizes):
+        raise InvalidInputError(f"group at frame {start}: a layer would be empty "
+                                f"({len(idx)} splats across {cfg.layer_count} layers)")
+    shdim = sh_coeff_count(key.sh_degree)
+    width = dict(_WIDTH, sh=shdim)
+    col0 = {"position": 0, "rotation": 3, "scales": 7, "opacity": 10, "sh": 11}
+    ncol = 11 + shdim
+    dev = torch.device("cuda", sess.device)
+    nf, n = len(frames), len(idx)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    chans = []  # (layer, attr, comp, bits, lo, hi, w, h)
+    for l in range(cfg.layer_count):
+        lo, hi = int(bounds[l]), int(bounds[l + 1])
+        w, h = _plane_shape(hi - lo)
+        if max(w, h, nf) > 0xFFFF:
+            raise InvalidInputError("plane run exceeds u16 geometry limits")
+        for attr in _ATTRS_SORTED:
+            for comp in range(width[attr]):
+                chans.append((l, attr, comp, position_bits if attr == "position" else 8, lo, hi, w, h))
+    with torch.cuda.stream(sess.stream):
+        d_idx = torch.from_numpy(np.ascontiguousarray(idx)).to(dev)
+        cols = torch.empty((ncol, nf, n), dtype=torch.float64, device=dev)  # significance order
+        for t, f in enumerate(frames):
+            for c0, a in ((0, f.positions), (3, f.rotations), (7, f.scales), (10, f.opacities), (11, f.sh)):
+                a = torch.from_numpy(np.ascontiguousarray(a, np.float64).reshape(len(f), -1)).to(dev)
+                cols[c0:c0 + a.shape[1], t, :] = a.index_select(0, d_idx).t()
+        rot = cols[3:7]
+        for t in range(1, nf):
+            p = rot[:, t] * rot[:, t - 1]
+            flip = torch.sign(((p[0] + p[1]) + p[2]) + p[3])
+            flip[flip == 0] = 1.0
+            rot[:, t] *= flip
+        offs, total = [], 0
+        for (_, _, _, bits, _, _, w, h) in chans:
+            offs.append(total)
+            total += (nf * w * h * (bits // 8) + 15) & ~15
+        planes = torch.empty(max(total, 16), dtype=torch.uint8, device=dev)
+        qc = (_lib.QuantChannel_t * len(chans))()
+        for i, (l, attr, comp, bits, lo, hi, w, h) in enumerate(chans):
+            qc[i] = _lib.QuantChannel_t(cols[col0[attr] + comp].data_ptr() + 8 * lo,
+                                        planes.data_ptr() + offs[i], n, nf, hi - lo, w, h, bits, 0.0, 0.0)
+        _lib.check(L.gsv_quantize_channels(sess.handle, qc, len(chans)))
+    ranges = [(float(q.range_min), float(q.range_max)) for q in qc]
+    return _PendingGroup(start=start, nf=nf, position_bits=position_bits, sizes=sizes, chans=chans,
+                         offs=offs, planes=planes, ranges=ranges, layer_count=cfg.layer_count)
+
+
+def _gpu_finish(pending: list, codecs: Sequence[int], sess) -> list:
+    """Second half: every run of every pending group range-coded in ONE
+    gsv_encode_runs call (runs are sequential inside, so parallelism comes
+    from the number of runs: batching groups is what fills the GPU), bodies
+    and raw planes read back once, payloads assembled (encode_planes,
+    codec.py:166-180)."""
+    import torch
+
+    from . import _lib
+    L = _lib.load()
+    items = [(g, i) for g in pending for i in range(len(g.chans))]
+    runs = (_lib.EncodeRun_t * max(len(items), 1))()
+    h_bodies = None
+    with torch.cuda.stream(sess.stream):
+        if 1 in codecs and items:
+            caps = [int(L.gsv_encode_body_capacity(g.nf, g.chans[i][6], g.chans[i][7], g.chans[i][3]))
+                    for g, i in items]
+            boffs = np.concatenate([[0], np.cumsum([(c + 15) & ~15 for c in caps])]).astype(np.int64)
+            bodies = torch.empty(int(boffs[-1]) + 16, dtype=torch.uint8, device=sess.device)
+            for k, (g, i) in enumerate(items):
+                _, _, _, bits, _, _, w, h = g.chans[i]
+                runs[k] = _lib.EncodeRun_t(g.planes.data_ptr() + g.offs[i], bodies.data_ptr() + int(boffs[k]),
+                                           g.nf, w, h, bits, 0, 0, 0)
+            _lib.check(L.gsv_encode_runs(sess.handle, runs, len(items)))
+            h_bodies = bodies.cpu().numpy()
+            del bodies
+        h_planes = {id(g): g.planes.cpu().numpy() for g in pending} if (0 in codecs or h_bodies is None) else {}
+    out = []
+    k = 0
+    for g in pending:
+        layers = [[] for _ in range(g.layer_count)]
+        for i, (l, attr, comp, bits, lo, hi, w, h) in enumerate(g.chans):
+            raw_len = g.nf * w * h * (bits // 8)
+            raw = h_planes[id(g)][g.offs[i]:g.offs[i] + raw_len].tobytes() if h_planes else None
+            crc = int(runs[k].checksum) if h_bodies is not None else zlib.crc32(raw) & 0xFFFFFFFF
+            payloads = {}
+            for c in codecs:
+                if c == 0:
+                    body = raw
+                elif c == 1:
+                    body = h_bodies[int(boffs[k]):int(boffs[k]) + int(runs[k].body_len)].tobytes()
+                else:
+                    raise InvalidInputError(f"encoder supports codec ids 0 and 1, got {c}")
+                payloads[c] = struct.pack("<BBHHHHI", c, bits, w, h, g.nf, 0, len(body)) + body + \
+                    struct.pack("<I", crc)
+            layers[l].append([attr, comp, bits, g.ranges[i][0], g.ranges[i][1], payloads])
+            k += 1
+        out.append(_Group(g.start, g.nf, g.position_bits, g.sizes, layers))
+    return out
+
+
+def _encode_group_gpu(frames: list, start: int, cfg: EncodeConfig, position_bits: int,
+                      codecs: Sequence[int], sess) -> _Group:
+    """_encode_group on the GPU (quantise + range-code one group)."""
+    return _gpu_finish([_gpu_quantize_group(frames, start, cfg, position_bits, sess)], codecs, sess)[0]
+
+
 def _serialize(groups: list, codec: int, cfg: EncodeConfig, sh_degree: int, bounds) -> bytes:
     L = cfg.layer_count
     dir_size = sum(8 + 4 * L + sum(2 + 28 * len(ents) for ents in g.layers) for g in groups)
@@ -228,11 +354,15 @@ def _serialize(groups: list, codec: int, cfg: EncodeConfig, sh_degree: int, boun
 
 def encode_stream(frame_source: Callable[[], Iterable[GaussianSet]], cfg: EncodeConfig, *,
                   codecs: Sequence[int] | None = None, threads: int | None = None,
-                  positions_source: Callable[[], Iterable[np.ndarray]] | None = None) -> dict:
+                  positions_source: Callable[[], Iterable[np.ndarray]] | None = None,
+                  device=None) -> dict:
     """Encode the sequence produced by `frame_source()` (called twice: a
     statistics pass for bounds / position width / group cuts, then the encode
     pass; `positions_source`, if given, replaces the first pass with a stream
-    of (N, 3) position arrays).  Returns {codec: container bytes}."""
+    of (N, 3) position arrays).  Returns {codec: container bytes}.
+
+    device: None encodes on host threads; True or an api.Session quantises
+    and range-codes on the GPU (_encode_group_gpu), with identical bytes."""
     from . import _lib
     lib = _lib.load()
     codecs = tuple(codecs) if codecs is not None else (int(cfg.codec),)
@@ -276,13 +406,28 @@ def encode_stream(frame_source: Callable[[], Iterable[GaussianSet]], cfg: Encode
     ends = cuts[1:] + [nframes]
     groups = []
     threads = threads or max(1, (os.cpu_count() or 1))
+    sess = None
+    if device is not None and device is not False:
+        from .api import Session
+        sess = device if isinstance(device, Session) else Session()
+    pending, pending_bytes = [], 0
+    batch_bytes = int(float(os.environ.get("GSV_ENC_BATCH_GB", "8")) * 2 ** 30)
     with ThreadPoolExecutor(max_workers=threads) as pool:
         buf, gi = [], 0
         for t, f in enumerate(frame_source()):
             buf.append(f)
             if t + 1 == ends[gi]:
-                groups.append(_encode_group(buf, cuts[gi], cfg, position_bits, codecs, pool, lib))
+                if sess is not None:  # quantise now, range-code in batches of groups
+                    pending.append(_gpu_quantize_group(buf, cuts[gi], cfg, position_bits, sess))
+                    pending_bytes += pending[-1].planes.numel()
+                    if pending_bytes > batch_bytes:
+                        groups.extend(_gpu_finish(pending, codecs, sess))
+                        pending, pending_bytes = [], 0
+                else:
+                    groups.append(_encode_group(buf, cuts[gi], cfg, position_bits, codecs, pool, lib))
                 buf, gi = [], gi + 1
+    if pending:
+        groups.extend(_gpu_finish(pending, codecs, sess))
     bounds = (*mins.tolist(), *maxs.tolist())
     return {c: _serialize(groups, c, cfg, sh_degree, bounds) for c in codecs}
 
