@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
-    uint8_t* __restrict__ out_rgb8) {
+    uint8_t* __restrict__ out_rgb8, bool pairskip) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
     __shared__ __align__(16) float4 s_rec[4][32 * 4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             const bool colin = px >= (int)(rx & 0xFFFFu) && px < (int)(rx >> 16);
             const int lo = min(max(y0 - py0, 0), ROWS), hi = min(max(y1 - py0, 0), ROWS);
             const uint32_t m = colin ? ((0xFFFFu << lo) & ~(0xFFFFu << hi)) : 0u;
-            if (!__any_sync(0xffffffffu, m & live)) continue;  // converged: lanes mask, not branch
+            // rows some lane still needs (rect and T >= 1e-4): one vote per
+            // record, then whole row pairs no lane needs are skipped with a
+            // warp-uniform branch (rect edges, saturated rows)
+            const uint32_t need = __reduce_or_sync(0xffffffffu, m & live);
+            if (!need) continue;
             const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
             const float op = r3.x;
@@ -208,6 +212,7 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
                 const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};
 #pragma unroll
                 for (int j = 0; j < ROWS; j += 2) {
+                    if (pairskip && !(need & (3u << j))) continue;
                     const f2 dy = add2(D2, f2{(float)j, (float)(j + 1)});
                     f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
                     pw.x = fminf(pw.x, pix_lim(m, 1u << j, T[j]));
@@ -307,6 +312,11 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
     const unsigned grid = (unsigned)((warps + 3) / 4);
+    static int pairskip = -1;  // dev toggle: skip row pairs no lane needs
+    if (pairskip < 0) {
+        const char* e = getenv("GSV_COMPOSITE_PAIRSKIP");
+        pairskip = e ? atoi(e) : 1;
+    }
     static int packed = -1;
     if (packed < 0) {
         const char* e = getenv("GSV_COMPOSITE_PACKED");
@@ -315,7 +325,7 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
 #define GSV_COMPOSITE(R, P)                                                                             \
     composite_strip_kernel<R, P><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
                                                       cam.height, ntx, ntiles, first, last, cam.bg[0],   \
-                                                      cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
+                                                      cam.bg[1], cam.bg[2], out_rgb, out_rgb8, pairskip)
     if (packed) {
         if (rows == 8) GSV_COMPOSITE(8, true);
         else if (rows == 4) GSV_COMPOSITE(4, true);
