@@ -12,6 +12,8 @@
 // it; the others carry their (C, T) to the next round through `state`, and
 // the last round finishes every tile still open.
 #include <stdint.h>
+
+#include <type_traits>
 #include <stdlib.h>
 
 #include "gsv_internal.h"
@@ -100,6 +102,16 @@ __device__ __forceinline__ float pix_lim(uint32_t m, uint32_t bit, float T) {
         : "=f"(r) : "r"(m), "r"(bit), "f"(T));
     return r;
 }
+// T if the pixel takes this splat (rect bit set and T >= 1e-4), else 0: a
+// zero weight leaves C and T unchanged, exactly like the reference's skip
+__device__ __forceinline__ float t_eff(uint32_t m, uint32_t bit, float T) {
+    float r;
+    asm("{\n\t.reg .pred pm, pt;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 pm, t, 0;\n\t"
+        "setp.ge.and.f32 pt, %3, 0f38D1B717, pm;\n\t"
+        "selp.f32 %0, %3, 0f00000000, pt;\n\t}"
+        : "=f"(r) : "r"(m), "r"(bit), "f"(T));
+    return r;
+}
 __device__ __forceinline__ float ex2f(float x) {
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
@@ -117,13 +129,13 @@ __device__ __forceinline__ float ex2f(float x) {
 // pixel), power clamp, 0.99 alpha cap, alpha <= 0 skip, fp32, fixed order.
 // The quadratic form is evaluated as A + dy (B + C dy) with A, B per
 // (record, column) -- a different fp32 rounding of the same fp64 quantity.
-template <int ROWS, bool PACKED>
+template <int ROWS, bool PACKED, bool TEFF>
 __global__ void __launch_bounds__(128) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
-    uint8_t* __restrict__ out_rgb8, bool pairskip) {
+    uint8_t* __restrict__ out_rgb8) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
     __shared__ __align__(16) float4 s_rec[4][32 * 4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -207,33 +219,55 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             if constexpr (PACKED) {
                 // row pairs; a pixel outside the rect or at T < 1e-4 gets power
                 // -inf (alpha 0: C, T unchanged); opacities are >= 0 (clamped
-                // in the record: a negative one draws nothing in the reference)
-                const f2 A2{A, A}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
+                // in the record: a negative one draws nothing in the reference).
+                // TEFF: such pixels get weight T_eff = 0 instead, and the
+                // opacity is folded into the exponent (A + log2 op, from the
+                // record), so alpha = 2^pw needs no multiply and, for op <=
+                // 0.99, no 0.99 cap (alpha <= op); the reference's p = min(p,
+                // 0) only trims rounding (the conic is positive definite)
+                const float A1 = TEFF ? A + __uint_as_float(__float_as_uint(r3.w)) : A;
+                const f2 A2{A1, A1}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
                 const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};
+                const f2 dy01 = add2(D2, f2{0.f, 1.f});
+                auto pairs = [&](auto cap_c) {
+                    constexpr bool CAP = decltype(cap_c)::value;
 #pragma unroll
-                for (int j = 0; j < ROWS; j += 2) {
-                    if (pairskip && !(need & (3u << j))) continue;
-                    const f2 dy = add2(D2, f2{(float)j, (float)(j + 1)});
-                    f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
-                    pw.x = fminf(pw.x, pix_lim(m, 1u << j, T[j]));
-                    pw.y = fminf(pw.y, pix_lim(m, 1u << (j + 1), T[j + 1]));
-                    f2 al = mul2(O2, f2{ex2f(pw.x), ex2f(pw.y)});
-                    al.x = fminf(al.x, 0.99f);
-                    al.y = fminf(al.y, 0.99f);
-                    const f2 w = mul2(f2{T[j], T[j + 1]}, al);
-                    f2 c = fma2(w, R2, f2{c0[j], c0[j + 1]});
-                    c0[j] = c.x;
-                    c0[j + 1] = c.y;
-                    c = fma2(w, G2, f2{c1[j], c1[j + 1]});
-                    c1[j] = c.x;
-                    c1[j + 1] = c.y;
-                    c = fma2(w, Bl2, f2{c2[j], c2[j + 1]});
-                    c2[j] = c.x;
-                    c2[j + 1] = c.y;
-                    const f2 t = fma2(w, M1, f2{T[j], T[j + 1]});  // T (1 - alpha)
-                    T[j] = t.x;
-                    T[j + 1] = t.y;
-                }
+                    for (int j = 0; j < ROWS; j += 2) {
+                        if (!(need & (3u << j))) continue;
+                        // (j, j) broadcast: an immediate operand, no pair constant to build
+                        const f2 dy = j ? add2(dy01, f2{(float)j, (float)j}) : dy01;
+                        f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
+                        f2 te, al;
+                        if (TEFF) {
+                            te = f2{t_eff(m, 1u << j, T[j]), t_eff(m, 1u << (j + 1), T[j + 1])};
+                            al = f2{ex2f(pw.x), ex2f(pw.y)};
+                        } else {
+                            pw.x = fminf(pw.x, pix_lim(m, 1u << j, T[j]));
+                            pw.y = fminf(pw.y, pix_lim(m, 1u << (j + 1), T[j + 1]));
+                            te = f2{T[j], T[j + 1]};
+                            al = mul2(O2, f2{ex2f(pw.x), ex2f(pw.y)});
+                        }
+                        if (CAP) {
+                            al.x = fminf(al.x, 0.99f);
+                            al.y = fminf(al.y, 0.99f);
+                        }
+                        const f2 w = mul2(te, al);
+                        f2 c = fma2(w, R2, f2{c0[j], c0[j + 1]});
+                        c0[j] = c.x;
+                        c0[j + 1] = c.y;
+                        c = fma2(w, G2, f2{c1[j], c1[j + 1]});
+                        c1[j] = c.x;
+                        c1[j + 1] = c.y;
+                        c = fma2(w, Bl2, f2{c2[j], c2[j + 1]});
+                        c2[j] = c.x;
+                        c2[j + 1] = c.y;
+                        const f2 t = fma2(w, M1, f2{T[j], T[j + 1]});  // T (1 - alpha)
+                        T[j] = t.x;
+                        T[j + 1] = t.y;
+                    }
+                };
+                if (TEFF && op <= 0.99f) pairs(std::false_type{});
+                else pairs(std::true_type{});
             } else {
                 // branch-free over the lane's rows: a pixel outside the rect or
                 // already at T < 1e-4 gets alpha 0, and alpha <= 0 composites as a
@@ -312,28 +346,25 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
     const unsigned grid = (unsigned)((warps + 3) / 4);
-    static int pairskip = -1;  // dev toggle: skip row pairs no lane needs
-    if (pairskip < 0) {
-        const char* e = getenv("GSV_COMPOSITE_PAIRSKIP");
-        pairskip = e ? atoi(e) : 1;
-    }
     static int packed = -1;
     if (packed < 0) {
         const char* e = getenv("GSV_COMPOSITE_PACKED");
-        packed = e ? atoi(e) : 1;
+        packed = e ? atoi(e) : 2;
     }
-#define GSV_COMPOSITE(R, P)                                                                             \
-    composite_strip_kernel<R, P><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
-                                                      cam.height, ntx, ntiles, first, last, cam.bg[0],   \
-                                                      cam.bg[1], cam.bg[2], out_rgb, out_rgb8, pairskip)
-    if (packed) {
-        if (rows == 8) GSV_COMPOSITE(8, true);
-        else if (rows == 4) GSV_COMPOSITE(4, true);
-        else GSV_COMPOSITE(2, true);
+#define GSV_COMPOSITE(R, P, E)                                                                          \
+    composite_strip_kernel<R, P, E><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
+                                                         cam.height, ntx, ntiles, first, last, cam.bg[0],   \
+                                                         cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
+    if (packed == 2 && rows == 8) {
+        GSV_COMPOSITE(8, true, true);
+    } else if (packed) {
+        if (rows == 8) GSV_COMPOSITE(8, true, false);
+        else if (rows == 4) GSV_COMPOSITE(4, true, false);
+        else GSV_COMPOSITE(2, true, false);
     } else {
-        if (rows == 8) GSV_COMPOSITE(8, false);
-        else if (rows == 4) GSV_COMPOSITE(4, false);
-        else GSV_COMPOSITE(2, false);
+        if (rows == 8) GSV_COMPOSITE(8, false, false);
+        else if (rows == 4) GSV_COMPOSITE(4, false, false);
+        else GSV_COMPOSITE(2, false, false);
     }
 #undef GSV_COMPOSITE
 }

@@ -151,13 +151,14 @@ struct CamDev {
 //                        (render.py:346-349): alpha = op * 2^(ca dx^2 + cb dx dy + cc dy^2)
 //   r, g, b            : SH colour in [0, 1];  op : opacity
 //   rx, ry             : x0 | x1 << 16, y0 | y1 << 16 (u16 each; tile binning)
+//   lop                : log2(op) as float bits (-inf for op = 0)
 struct __align__(16) SplatRec {
     float fx0, fy0, fx1, fy1;
     float ox, oy, ca, cb;
     float cc, r, g, b;
     float op;
     uint32_t rx, ry;
-    uint32_t pad;
+    uint32_t pad;  // lop
 };
 
 // ---- workspace for one in-flight render ----------------------------------

@@ -353,9 +353,9 @@ __global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
             r.g = (float)rgb[1];
             r.b = (float)rgb[2];
             r.op = (float)np_max(a.o, 0.0);  // alpha <= 0 draws nothing (render.py:326)
+            r.pad = __float_as_uint(r.op > 0.f ? log2f(r.op) : -INFINITY);  // log2 op for the compositor
             r.rx = (uint32_t)o.x0 | ((uint32_t)o.x1 << 16);
             r.ry = (uint32_t)o.y0 | ((uint32_t)o.y1 << 16);
-            r.pad = 0;
             rec[i] = r;
         }
         if (dbg_rect) {
@@ -469,9 +469,9 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
             r.g = (float)colors[3 * i + 1];
             r.b = (float)colors[3 * i + 2];
             r.op = (float)np_max(opac[i], 0.0);  // alpha <= 0 draws nothing (render.py:326)
+            r.pad = __float_as_uint(r.op > 0.f ? log2f(r.op) : -INFINITY);
             r.rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             r.ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
-            r.pad = 0;
             rec[i] = r;
         }
         dkey[i] = key;
