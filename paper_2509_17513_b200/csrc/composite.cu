@@ -155,7 +155,11 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const int px = tx * kTile + (lane & 15);
     const int sy0 = ty * kTile + strip * 2 * ROWS;  // strip's first row
     const int py0 = sy0 + (lane >> 4) * ROWS;        // this lane's first row
-    const float pxf = (float)px, py0f = (float)py0;
+    // lane constants against the staged per-(record, tile) fields below
+    const float colf = (float)(lane & 15);                          // column in the tile
+    const int rowoff = strip * 2 * ROWS + (lane >> 4) * ROWS;       // first row in the tile
+    const float rowf = (float)rowoff;
+    const uint32_t colsh = (uint32_t)(lane & 15), rowsh = 16u + (uint32_t)rowoff;
     float T[ROWS], c0[ROWS], c1[ROWS], c2[ROWS];
     uint32_t live = 0, inimg = 0;
     const bool work = on && start < end;
@@ -184,27 +188,35 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
         if (!__any_sync(0xffffffffu, live)) break;
         const uint32_t jr = base + lane;
         if (jr < end) {
+            // stage the record with its tile-relative fields precomputed once
+            // per (record, tile) instead of per lane and record: slot 0 =
+            // (bx, by, mask) with dx = column + bx, dy = row + by and mask =
+            // the rect's columns (bits 0-15) and rows (bits 16-31) in the tile
             const float4* r = reinterpret_cast<const float4*>(recs + __ldg(ranks + jr));
-#pragma unroll
-            for (int k = 0; k < 4; k++) s_rec[warp][lane * 4 + k] = __ldg(r + k);
+            const float4 v0 = __ldg(r), v1 = __ldg(r + 1), v2 = __ldg(r + 2), v3 = __ldg(r + 3);
+            const uint32_t rx = __float_as_uint(v3.y), ry = __float_as_uint(v3.z);
+            const int tx0 = tx * kTile, ty0 = ty * kTile;
+            const int cl = min(max((int)(rx & 0xFFFFu) - tx0, 0), 16), ch = min(max((int)(rx >> 16) - tx0, 0), 16);
+            const int rl = min(max((int)(ry & 0xFFFFu) - ty0, 0), 16), rh = min(max((int)(ry >> 16) - ty0, 0), 16);
+            const uint32_t cm = (0xFFFFu << cl) & ~(0xFFFFu << ch) & 0xFFFFu;
+            const uint32_t rm = (0xFFFFu << rl) & ~(0xFFFFu << rh) & 0xFFFFu;
+            s_rec[warp][lane * 4] = make_float4(((float)tx0 - v0.x) - v1.x, ((float)ty0 - v0.y) - v1.y,
+                                                __uint_as_float(cm | (rm << 16)), 0.f);
+            s_rec[warp][lane * 4 + 1] = v1;
+            s_rec[warp][lane * 4 + 2] = v2;
+            s_rec[warp][lane * 4 + 3] = v3;
         }
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
         for (int q = 0; q < cnt; q++) {
             const uint32_t ra = sbase + (uint32_t)q * 64u;
-            const float4 rc = lds_f4(ra);        // x0, y0, x1, y1 as floats (exact integers)
-            const float4 r3 = lds_f4(ra + 48u);  // op, rx = x0 | x1 << 16, ry = y0 | y1 << 16
-            const uint32_t rx = __float_as_uint(r3.y), ry = __float_as_uint(r3.z);
-            const int y0 = (int)(ry & 0xFFFFu), y1 = (int)(ry >> 16);
-            // strip rows [sy0, sy0 + 2 ROWS) against [y0, y1): warp-uniform skip
-            // (a strip of 8-row lanes is the whole tile: every record overlaps it)
-            if (kStrips > 1 && (y0 >= sy0 + 2 * ROWS || y1 <= sy0)) continue;
-            // rows of the lane's column inside the rect (empty outside its columns);
-            // integer rect from the record: no float->int conversions on the
-            // SFU pipe the ex2s need
-            const bool colin = px >= (int)(rx & 0xFFFFu) && px < (int)(rx >> 16);
-            const int lo = min(max(y0 - py0, 0), ROWS), hi = min(max(y1 - py0, 0), ROWS);
-            const uint32_t m = colin ? ((0xFFFFu << lo) & ~(0xFFFFu << hi)) : 0u;
+            const float4 rc = lds_f4(ra);  // bx, by, column | row mask of the rect in this tile
+            const uint32_t mw = __float_as_uint(rc.z);
+            // strip rows against the rect: warp-uniform skip (a strip of 8-row
+            // lanes is the whole tile: every record overlaps it)
+            if (kStrips > 1 && ((mw >> (16 + strip * 2 * ROWS)) & ((1u << (2 * ROWS)) - 1u)) == 0u) continue;
+            // rows of the lane's column inside the rect (empty outside its columns)
+            const uint32_t m = ((mw >> colsh) & 1u) ? (mw >> rowsh) & ((1u << ROWS) - 1u) : 0u;
             // rows some lane still needs (rect and T >= 1e-4): one vote per
             // record, then whole row pairs no lane needs are skipped with a
             // warp-uniform branch (rect edges, saturated rows)
@@ -212,10 +224,11 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             if (!need) continue;
             const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
+            const float4 r3 = lds_f4(ra + 48u);  // op, rx, ry, log2 op
             const float op = r3.x;
-            const float dx = (pxf - rc.x) - a.x;
+            const float dx = colf + rc.x;
             const float A = a.z * dx * dx, B = a.w * dx;
-            const float dy0 = (py0f - rc.y) - a.y;
+            const float dy0 = rowf + rc.y;
             if constexpr (PACKED) {
                 // row pairs; a pixel outside the rect or at T < 1e-4 gets power
                 // -inf (alpha 0: C, T unchanged); opacities are >= 0 (clamped
