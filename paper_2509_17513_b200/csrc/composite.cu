@@ -112,6 +112,9 @@ __device__ __forceinline__ float t_eff(uint32_t m, uint32_t bit, float T) {
         : "=f"(r) : "r"(m), "r"(bit), "f"(T));
     return r;
 }
+__device__ __forceinline__ void sts_f4(uint32_t addr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
 __device__ __forceinline__ float ex2f(float x) {
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
     uint8_t* __restrict__ out_rgb8) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
-    __shared__ __align__(16) float4 s_rec[4][32 * 4];
+    __shared__ __align__(16) float4 s_rec[2][4][32 * 4];  // double-buffered per-warp batches
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw = blockIdx.x * 4 + warp;
     const int tile = gw / kStrips, strip = gw % kStrips;
@@ -183,28 +186,55 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
             if (T[j] >= 1e-4f) live |= 1u << j;
         }
     }
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(&s_rec[warp][0]);
-    for (uint32_t base = start; work && base < end; base += 32) {
-        if (!__any_sync(0xffffffffu, live)) break;
-        const uint32_t jr = base + lane;
+    // records arrive by cp.async one batch (32 records) ahead, double
+    // buffered per warp; the rank of the batch after that is loaded a batch
+    // ahead too, so neither the rank nor the record gather sits in front of
+    // the compositing (round 2's few open tiles are latency-bound)
+    const uint32_t sb[2] = {(uint32_t)__cvta_generic_to_shared(&s_rec[0][warp][0]),
+                            (uint32_t)__cvta_generic_to_shared(&s_rec[1][warp][0])};
+    auto issue = [&](uint32_t dst, uint32_t jr, uint32_t rank) {
         if (jr < end) {
-            // stage the record with its tile-relative fields precomputed once
-            // per (record, tile) instead of per lane and record: slot 0 =
-            // (bx, by, mask) with dx = column + bx, dy = row + by and mask =
-            // the rect's columns (bits 0-15) and rows (bits 16-31) in the tile
-            const float4* r = reinterpret_cast<const float4*>(recs + __ldg(ranks + jr));
-            const float4 v0 = __ldg(r), v1 = __ldg(r + 1), v2 = __ldg(r + 2), v3 = __ldg(r + 3);
+            const char* src = reinterpret_cast<const char*>(recs + rank);
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + lane * 64u + 16u * k),
+                             "l"(src + 16 * k));
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    uint32_t rank_nx = 0;
+    if (work) {
+        issue(sb[0], start + lane, start + lane < end ? __ldg(ranks + start + lane) : 0u);
+        rank_nx = start + 32 + lane < end ? __ldg(ranks + start + 32 + lane) : 0u;
+    }
+    int it = 0;
+    for (uint32_t base = start; work && base < end; base += 32, it++) {
+        if (!__any_sync(0xffffffffu, live)) break;
+        const uint32_t sbase = sb[it & 1];
+        const bool more = base + 32 < end;
+        if (more) {
+            issue(sb[(it + 1) & 1], base + 32 + lane, rank_nx);
+            rank_nx = base + 64 + lane < end ? __ldg(ranks + base + 64 + lane) : 0u;
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        if (base + lane < end) {
+            // tile-relative fields once per (record, tile) instead of per lane
+            // and record: slot 0 = (bx, by, mask) with dx = column + bx, dy =
+            // row + by, mask = the rect's columns (bits 0-15) and rows (bits
+            // 16-31) in this tile
+            const uint32_t sl = sbase + lane * 64u;
+            const float4 v0 = lds_f4(sl), v1 = lds_f4(sl + 16u), v3 = lds_f4(sl + 48u);
             const uint32_t rx = __float_as_uint(v3.y), ry = __float_as_uint(v3.z);
             const int tx0 = tx * kTile, ty0 = ty * kTile;
             const int cl = min(max((int)(rx & 0xFFFFu) - tx0, 0), 16), ch = min(max((int)(rx >> 16) - tx0, 0), 16);
             const int rl = min(max((int)(ry & 0xFFFFu) - ty0, 0), 16), rh = min(max((int)(ry >> 16) - ty0, 0), 16);
             const uint32_t cm = (0xFFFFu << cl) & ~(0xFFFFu << ch) & 0xFFFFu;
             const uint32_t rm = (0xFFFFu << rl) & ~(0xFFFFu << rh) & 0xFFFFu;
-            s_rec[warp][lane * 4] = make_float4(((float)tx0 - v0.x) - v1.x, ((float)ty0 - v0.y) - v1.y,
-                                                __uint_as_float(cm | (rm << 16)), 0.f);
-            s_rec[warp][lane * 4 + 1] = v1;
-            s_rec[warp][lane * 4 + 2] = v2;
-            s_rec[warp][lane * 4 + 3] = v3;
+            sts_f4(sl, make_float4(((float)tx0 - v0.x) - v1.x, ((float)ty0 - v0.y) - v1.y,
+                                   __uint_as_float(cm | (rm << 16)), 0.f));
         }
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
@@ -311,6 +341,7 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
         live &= inimg;
         __syncwarp();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     const bool tsat = __all_sync(0xffffffffu, (live & inimg) == 0);
     if (!on) return;
     // finish the strip (background blend, clip: render.py:333-338, 356) when
