@@ -8,4 +8,6 @@ for k in composite_strip radix_onesweep round_emit_fused project_kernel gather_s
      -o gpurun_out/prof/full_$k python tools/ncu_driver.py 0 > gpurun_out/prof/full_$k.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_decode -c 1 \
-     -o gpurun_out/prof/full_rc_decode python tools/rc_bench.py --planes 3 2 > gpurun_out/prof/full_rc_decode.log 2>&1
+     -o gpurun_out/prof/full_rc_decode python tools/rc_bench.py --planes 3 3 > gpurun_out/prof/full_rc_decode.log 2>&1
+ENC_N=50000 ENC_FRAMES=30 ENC_SKIP_HOST=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_encode -c 1 \
+     -o gpurun_out/prof/full_rc_encode python tools/enc_bench.py > gpurun_out/prof/full_rc_encode.log 2>&1
