@@ -397,7 +397,8 @@ void launch_rc_encode(const EncRun* d_runs, const uint32_t* d_order, const int* 
     }
     if (c.blk[3] == 0) return;
     const size_t smem = (size_t)enc_lane_stride(nbmax) * lanes;
-    if (lanes <= 4) {
+    const char* eb = getenv("GSV_ENC_BRANCHY");  // dev override: 1 branchy, 0 predicated
+    if (eb ? atoi(eb) != 0 : lanes <= 4) {
         cudaFuncSetAttribute(rc_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         rc_encode_kernel<true><<<c.blk[3], kEncRPW, smem, s>>>(d_runs, d_order, c, d_res);
     } else {
