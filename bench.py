@@ -390,7 +390,7 @@ def run_b200(a, rank, world, dist):
         e2e = {"value": round(f, 2), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(a.frames * a.width * a.height * 3),
                "path": "per-group DeviceVideo(host, groups=(g, g+1)) + render_batch(host_u8), "
-                       "3 host threads / sessions",
+                       f"{os.environ.get('GSV_E2E_WORKERS', '4')} host threads / sessions",
                "whole_container_open_fps": round(timed_e2e_pipelined.whole_fps, 2),
                "pcie_floor_ms_per_step": "H2D 42 + D2H 34 concurrently 51 (tools/pcie_probe.py)"}
 
@@ -450,7 +450,7 @@ def timed_e2e_pipelined(a, gsvb, sess, blob, cs, steps, warmup, dist):
     for g in info.groups:
         starts.append(acc)
         acc += g.frame_count
-    nw = int(os.environ.get("GSV_E2E_WORKERS", "3"))
+    nw = int(os.environ.get("GSV_E2E_WORKERS", "4"))
     sessions = [sess] + [gsvb.Session(sess.device) for _ in range(nw - 1)]
     from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(max_workers=nw)
