@@ -145,3 +145,32 @@ def test_gpu_quantizer_matches_numpy(sess):
         assert (float(qc[0].range_min), float(qc[0].range_max)) == (rmin, rmax)
         got = planes.cpu().numpy().view(want.dtype).reshape(want.shape)
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("case", ["prune_fractions", "fixed_groups_deg3", "deg0_wide", "large_motion"])
+def test_gpu_encoder_matches_host_encoder(sess, case):
+    """Encoder options the fixtures do not pin (pruning, custom layer
+    fractions, fixed group lengths, SH degrees 0 and 3, 32-bit positions,
+    strong motion that cuts many groups): GPU bytes == host bytes, both
+    codecs."""
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.synth import SceneSpec, iter_frames
+    if case == "prune_fractions":
+        spec = SceneSpec(count=5000, frames=6, sh_degree=1, amplitude=0.002, rotation_amplitude=0.02,
+                         scale_amplitude=0.001, opacity_amplitude=0.01, sh_amplitude=0.01)
+        cfg = EncodeConfig(layer_count=3, layer_fractions=(0.2, 0.3, 0.5), prune_fraction=0.4)
+    elif case == "fixed_groups_deg3":
+        spec = SceneSpec(count=3000, frames=7, sh_degree=3, amplitude=0.001, rotation_amplitude=0.05,
+                         scale_amplitude=0.001, opacity_amplitude=0.02, sh_amplitude=0.02)
+        cfg = EncodeConfig(layer_count=4, prune_fraction=0.1, fixed_group_length=3)
+    elif case == "deg0_wide":
+        spec = SceneSpec(count=2000, frames=4, sh_degree=0, amplitude=0.5, position_extent=80.0)
+        cfg = EncodeConfig(layer_count=2, prune_fraction=0.0)
+    else:
+        spec = SceneSpec(count=4000, frames=8, sh_degree=1, amplitude=0.02, rotation_amplitude=0.3,
+                         scale_amplitude=0.01, opacity_amplitude=0.1, sh_amplitude=0.1)
+        cfg = EncodeConfig(layer_count=6, prune_fraction=0.0)
+    host = encode_stream(lambda: iter_frames(spec, 11), cfg, codecs=(0, 1), threads=4)
+    gpu = encode_stream(lambda: iter_frames(spec, 11), cfg, codecs=(0, 1), device=sess)
+    assert gpu[0] == host[0]
+    assert gpu[1] == host[1]
