@@ -76,6 +76,19 @@ __global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ct
     reinterpret_cast<int*>(ctr + C_NPASS)[1] = 0;
 }
 
+// Significant bits of the rebased depth key the radix sort runs on (24:
+// three passes; ties of the truncated key are put in exact order by
+// depth_tie_fixup).  GSV_DEPTH_KEY_BITS (16, 24 or 32) for dev tuning.
+static int depth_key_bits() {
+    static int b = 0;
+    if (!b) {
+        const char* e = getenv("GSV_DEPTH_KEY_BITS");
+        b = e ? atoi(e) : 24;
+        if (b != 16 && b != 24 && b != 32) b = 24;
+    }
+    return b;
+}
+
 // Rebase survivor depth bits to [0, range]; culled splats get range + 1 (so
 // they sort last).  The radix sort runs on the top 32 significant bits of
 // that key (key32); full[] keeps the 64-bit key by splat index for the
@@ -84,7 +97,7 @@ __global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ct
 // radix_hist, sort.cuh).
 __global__ void __launch_bounds__(256) depth_key_prep(uint64_t* __restrict__ full, uint32_t* __restrict__ key32,
                                                       unsigned long long* __restrict__ ctr,
-                                                      uint32_t* __restrict__ ghist) {
+                                                      uint32_t* __restrict__ ghist, int keybits) {
     __shared__ uint32_t h[4][256];
 #pragma unroll
     for (int p = 0; p < 4; p++) h[p][threadIdx.x] = 0;
@@ -94,7 +107,7 @@ __global__ void __launch_bounds__(256) depth_key_prep(uint64_t* __restrict__ ful
     const uint64_t lo = ctr[C_DMIN], hi = ctr[C_DMAX];
     const uint64_t dead = nvis ? (hi - lo) + 1 : 0;
     const int bits = dead ? 64 - __clzll((long long)dead) : 0;
-    const int shift = bits > 32 ? bits - 32 : 0;
+    const int shift = bits > keybits ? bits - keybits : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const int kb = bits - shift;
         reinterpret_cast<int*>(ctr + C_NPASS)[0] = (nvis == 0 || (nvis == n && hi == lo)) ? 0 : (kb + 7) / 8;
@@ -570,13 +583,15 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     count_launch(2);
     prof_mark(ST_DSORT, s);
     if (n > 0) {
-        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
-        if (!(skip & 4)) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
-        if (dbl & 4) radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
+        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist, depth_key_bits());
+        if (!(skip & 4))
+            radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
+        if (dbl & 4)
+            radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         if (dbl & 64)
             depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
-        count_launch(2 + radix_launches(4, true));
+        count_launch(2 + radix_launches(depth_key_bits() / 8, true));
     }
     prof_mark(ST_EMIT, s);
     const unsigned g = 148 * 4;
@@ -850,8 +865,8 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
                                           0u);
     launch_project_soa(src, cam, w, rects, depth, s);
     if (n > 0) {
-        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist);
-        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, 4, npass, sc.ghist, sc, s);
+        depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist, depth_key_bits());
+        radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
         depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
         copy_order<<<148 * 4, 256, 0, s>>>(w->didx[0], w->didx[1], ctr, order, w->rec, tile_count);
     }
