@@ -390,7 +390,7 @@ def run_b200(a, rank, world, dist):
         e2e = {"value": round(f, 2), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(a.frames * a.width * a.height * 3),
                "path": "per-group DeviceVideo(host, groups=(g, g+1)) + render_batch(host_u8), "
-                       f"{os.environ.get('GSV_E2E_WORKERS', '4')} host threads / sessions",
+                       f"{os.environ.get('GSV_E2E_WORKERS', '3')} host threads / sessions",
                "whole_container_open_fps": round(timed_e2e_pipelined.whole_fps, 2),
                "pcie_floor_ms_per_step": "H2D 42 + D2H 34 concurrently 51 (tools/pcie_probe.py)"}
 
@@ -450,32 +450,33 @@ def timed_e2e_pipelined(a, gsvb, sess, blob, cs, steps, warmup, dist):
     for g in info.groups:
         starts.append(acc)
         acc += g.frame_count
-    nw = int(os.environ.get("GSV_E2E_WORKERS", "4"))
+    nw = int(os.environ.get("GSV_E2E_WORKERS", "3"))
     sessions = [sess] + [gsvb.Session(sess.device) for _ in range(nw - 1)]
     from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(max_workers=nw)
 
     import threading
-    first_open = threading.Event()
+    first_open = [threading.Event() for _ in range(nw)]
 
     def worker(w, verify):
-        # host thread w drives session w over groups w, w+2, ... (the C ABI
-        # releases the GIL); thread 1 starts once thread 0's first group is
-        # open, so the two alternate: one uploads + validates while the other
-        # renders and reads back
+        # host thread w drives session w over groups w, w+nw, ... (the C ABI
+        # releases the GIL); thread w starts once thread w-1's first group is
+        # open, so the uploads are staggered (one at a time at full PCIe rate)
+        # instead of bunching up while no frame renders
         torch.cuda.set_device(sess.device)
         if w > 0:
-            first_open.wait()
+            first_open[w - 1].wait()
         for gi in range(w, len(info.groups), nw):
             g = info.groups[gi]
             v = gsvb.DeviceVideo(host, a.k, session=sessions[w], groups=(gi, gi + 1), info=info)
-            first_open.set()
+            first_open[w].set()
             hf = [pinned[starts[gi] + i] for i in range(g.frame_count)]
             v.render_batch(list(range(g.frame_count)), cs, host_u8=hf, streams=a.streams, verify=verify)
             v.close()
 
     def one(verify=False):
-        first_open.clear()
+        for e in first_open:
+            e.clear()
         for f in [pool.submit(worker, w, verify) for w in range(nw)]:
             f.result()
 
