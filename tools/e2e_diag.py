@@ -16,19 +16,21 @@ cs = _lib.camera_struct(bench.camera(a))
 info = gsvb.read_structure(blob)
 host = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
 pinned = torch.empty((a.frames, a.height, a.width, 3), dtype=torch.uint8).pin_memory()
-sessions = [gsvb.Session(0), gsvb.Session(0)]
+import os
+NW = int(os.environ.get('NW', '4'))
+sessions = [gsvb.Session(0) for _ in range(NW)]
 log = []
 T0 = [0.0]
 def ev(*x): log.append((time.perf_counter() - T0[0], threading.get_ident() % 100) + x)
-first = threading.Event()
+first = [threading.Event() for _ in range(NW)]
 def worker(w, verify):
     torch.cuda.set_device(0)
-    if w == 1: first.wait()
-    for gi in range(w, len(info.groups), 2):
+    if w >= 1: first[w - 1].wait()
+    for gi in range(w, len(info.groups), NW):
         g = info.groups[gi]
         ev("open", gi)
         v = gsvb.DeviceVideo(host, a.k, session=sessions[w], groups=(gi, gi + 1), info=info)
-        first.set()
+        first[w].set()
         ev("opened", gi)
         hf = [pinned[gi * 30 + i] for i in range(g.frame_count)]
         v.render_batch(list(range(g.frame_count)), cs, host_u8=hf, streams=a.streams, verify=verify)
@@ -36,10 +38,10 @@ def worker(w, verify):
         v.close()
         ev("closed", gi)
 from concurrent.futures import ThreadPoolExecutor
-pool = ThreadPoolExecutor(2)
+pool = ThreadPoolExecutor(NW)
 for it in range(3):
-    log.clear(); first.clear(); torch.cuda.synchronize(); T0[0] = time.perf_counter()
-    for f in [pool.submit(worker, w, it == 0) for w in (0, 1)]: f.result()
+    log.clear(); [e.clear() for e in first]; torch.cuda.synchronize(); T0[0] = time.perf_counter()
+    for f in [pool.submit(worker, w, it == 0) for w in range(NW)]: f.result()
     torch.cuda.synchronize()
     tot = time.perf_counter() - T0[0]
 print(f"step {tot*1e3:.1f} ms")
