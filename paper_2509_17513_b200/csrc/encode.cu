@@ -136,6 +136,8 @@ __device__ __forceinline__ void e_sts(uint32_t addr, uint32_t v) {
 // encoder state of one plane (_rc.py:62-68)
 struct RcEncState {
     unsigned long long low;
+    unsigned long long whi;  // deferred mode: bits 64..127 of the low window
+    uint32_t s;              // deferred mode: renormalisation bytes not yet emitted
     uint32_t rng, cache;
     uint64_t cache_size;
     uint64_t npos;   // bytes emitted (written while < cap)
@@ -205,11 +207,82 @@ __device__ __forceinline__ void shift_low_br(RcEncState& st) {
     st.low = (unsigned long long)(lo32 & 0x00FFFFFFu) << 8;
 }
 
+// Deferred emission: renormalisation only shifts a 128-bit low window
+// (whi:low) and counts the byte; every 4 decisions the pending bytes are
+// pushed through shift_low's cache / 0xFF-run logic at once.  The emitted
+// stream is the digit string of the same big-number sum (carries that the
+// eager coder applies to its cache byte have already propagated inside the
+// window), so the bytes are identical, and the decision loop has no
+// branches on the renormalisation.  At most 2 bytes per decision, flushed
+// every 4 decisions: the window holds 33 + 64 bits.
+__device__ __forceinline__ uint64_t win_shr(const RcEncState& st, uint32_t a) {  // 32 <= a <= 96
+    return a >= 64 ? (st.whi >> (a - 64)) : ((st.low >> a) | (st.whi << (64 - a)));
+}
+__device__ __forceinline__ void flush_deferred(RcEncState& st) {
+    const uint32_t s = st.s;
+    if (s == 0) return;
+    uint32_t carry = (uint32_t)(win_shr(st, 32 + 8 * s) & 1u);
+    for (uint32_t i = 0; i < s; i++) {
+        if (st.npos + st.cache_size > st.limit) {
+            st.overflow = true;
+            break;
+        }
+        const uint32_t t = (uint32_t)(win_shr(st, 32 + 8 * (s - 1 - i)) & 0xFFu);
+        if (t != 0xFFu || carry != 0u) {
+            const uint32_t b = (st.cache + carry) & 0xFFu;
+            if (st.npos < st.cap) st.dst[st.npos] = (uint8_t)b;
+            st.zrun = b ? 0 : st.zrun + 1;
+            st.npos++;
+            if (st.cache_size > 1) {
+                const uint32_t bf = (0xFFu + carry) & 0xFFu;
+                st.npos = emit_run(st.dst, st.npos, st.cap, st.cache_size - 1, bf);
+                st.zrun = bf ? 0 : st.zrun + st.cache_size - 1;
+            }
+            st.cache = t;
+            st.cache_size = 0;
+        }
+        st.cache_size++;
+        carry = 0;
+    }
+    st.low &= 0xFFFFFFFFull;
+    st.whi = 0;
+    st.s = 0;
+}
+
+__device__ __forceinline__ void encode_byte_deferred(uint32_t T, uint32_t byte, RcEncState& st) {
+    uint32_t p[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) p[k] = e_lds(T + 4u * ((256u | byte) >> (8 - k)));
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t bit = (byte >> (7 - k)) & 1u;
+        const uint32_t bound = (st.rng >> 12) * p[k];
+        const unsigned long long add = bit ? bound : 0u;
+        st.low += add;
+        st.whi += st.low < add ? 1u : 0u;
+        st.rng = bit ? st.rng - bound : bound;
+        e_sts(T + 4u * ((256u | byte) >> (8 - k)),
+              p[k] + (uint32_t)(((int32_t)(bit ? 15u : 4096u) - (int32_t)p[k]) >> 4));
+        const bool r1 = st.rng < (1u << 24);
+        st.rng = r1 ? st.rng << 8 : st.rng;
+        st.whi = r1 ? (st.whi << 8) | (st.low >> 56) : st.whi;
+        st.low = r1 ? st.low << 8 : st.low;
+        st.s += r1 ? 1u : 0u;
+        if (st.rng < (1u << 24)) {  // rare second byte (rng < 2^16 after the decision)
+            st.rng <<= 8;
+            st.whi = (st.whi << 8) | (st.low >> 56);
+            st.low <<= 8;
+            st.s++;
+        }
+        if (k == 3 || k == 7) flush_deferred(st);
+    }
+}
+
 // one byte through tree T (_rc.py:76-97).  The path is known, so all 8
 // node probabilities are loaded up front; the decisions are unrolled and
-// only rng -> bound -> rng is serial.  BRANCHY: renormalise in a branch
+// only rng -> bound -> rng is serial.  MODE 1: renormalise in a branch
 // (few runs per warp) or predicated (full warps).
-template <bool BRANCHY>
+template <int MODE>
 __device__ __forceinline__ void encode_byte(uint32_t T, uint32_t byte, RcEncState& st) {
     uint32_t p[8];
 #pragma unroll
@@ -222,7 +295,7 @@ __device__ __forceinline__ void encode_byte(uint32_t T, uint32_t byte, RcEncStat
         st.rng = bit ? st.rng - bound : bound;
         e_sts(T + 4u * ((256u | byte) >> (8 - k)),
               p[k] + (uint32_t)(((int32_t)(bit ? 15u : 4096u) - (int32_t)p[k]) >> 4));
-        if (BRANCHY) {
+        if (MODE == 1) {
             while (st.rng < (1u << 24)) {
                 shift_low_br(st);
                 st.rng <<= 8;
@@ -246,7 +319,7 @@ __device__ __forceinline__ uint32_t ld_sample(const uint8_t* plane, uint32_t i) 
     return __ldg(reinterpret_cast<const uint32_t*>(plane) + i);
 }
 
-template <int NB, bool BRANCHY>
+template <int NB, int MODE>
 __device__ void encode_run(const EncRun& r, uint32_t P, EncResult* res) {
     for (int b = 0; b < NB; b++)  // new_bittree_probs (_rc.py:304-317)
         for (uint32_t i = 0; i < 256; i++)
@@ -264,6 +337,8 @@ __device__ void encode_run(const EncRun& r, uint32_t P, EncResult* res) {
         const uint8_t* prev = f > 0 ? plane - raw_plane : plane;
         RcEncState st;
         st.low = 0;
+        st.whi = 0;
+        st.s = 0;
         st.rng = 0xFFFFFFFFu;
         st.cache = 0;
         st.cache_size = 1;
@@ -295,12 +370,16 @@ __device__ void encode_run(const EncRun& r, uint32_t P, EncResult* res) {
             const uint32_t d = (v - pred) & mask;
             const uint32_t z = d < half ? 2u * d : 2u * ((0u - d) & mask) - 1u;
 #pragma unroll 1
-            for (int b = 0; b < NB; b++) encode_byte<BRANCHY>(P + b * kEncTree, (z >> (8 * b)) & 0xFFu, st);
+            for (int b = 0; b < NB; b++) {
+                if (MODE == 2) encode_byte_deferred(P + b * kEncTree, (z >> (8 * b)) & 0xFFu, st);
+                else encode_byte<MODE>(P + b * kEncTree, (z >> (8 * b)) & 0xFFu, st);
+            }
             if (++x == w) {
                 x = 0;
                 y++;
             }
         }
+        if (MODE == 2) flush_deferred(st);
         for (int i = 0; i < 5; i++) shift_low(st, !st.overflow);
         const int64_t n = st.overflow ? -1 : (int64_t)(st.npos - st.zrun);
         if (n < 0 || (uint64_t)n + 4 >= raw_plane) {
@@ -330,7 +409,7 @@ __device__ void encode_run(const EncRun& r, uint32_t P, EncResult* res) {
 // runs per warp (c.lanes) adapts to the run count: few runs -> one run per
 // warp (no divergence, branchy renormalisation), many runs -> full warps
 // (predicated renormalisation)
-template <bool BRANCHY>
+template <int MODE>
 __global__ void __launch_bounds__(kEncRPW) rc_encode_kernel(const EncRun* __restrict__ runs,
                                                             const uint32_t* __restrict__ order, EncClasses c,
                                                             EncResult* __restrict__ res) {
@@ -344,9 +423,9 @@ __global__ void __launch_bounds__(kEncRPW) rc_encode_kernel(const EncRun* __rest
     const uint32_t ri = order[c.off[cls] + gi];
     const uint32_t P = (uint32_t)__cvta_generic_to_shared(eprobs_s) + threadIdx.x * enc_lane_stride(nb);
     const EncRun r = runs[ri];
-    if (nb == 1) encode_run<1, BRANCHY>(r, P, res + ri);
-    else if (nb == 2) encode_run<2, BRANCHY>(r, P, res + ri);
-    else encode_run<4, BRANCHY>(r, P, res + ri);
+    if (nb == 1) encode_run<1, MODE>(r, P, res + ri);
+    else if (nb == 2) encode_run<2, MODE>(r, P, res + ri);
+    else encode_run<4, MODE>(r, P, res + ri);
 }
 
 // raw blocks: the RAW planes of coded runs, and every plane of whole-raw
@@ -397,14 +476,20 @@ void launch_rc_encode(const EncRun* d_runs, const uint32_t* d_order, const int* 
     }
     if (c.blk[3] == 0) return;
     const size_t smem = (size_t)enc_lane_stride(nbmax) * lanes;
-    const char* eb = getenv("GSV_ENC_BRANCHY");  // dev override: 1 branchy, 0 predicated
-    if (eb ? atoi(eb) != 0 : lanes <= 4) {
-        cudaFuncSetAttribute(rc_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_encode_kernel<true><<<c.blk[3], kEncRPW, smem, s>>>(d_runs, d_order, c, d_res);
+    // renormalisation: 2 deferred (default), 1 branchy, 0 predicated (dev: GSV_ENC_MODE)
+    const char* em = getenv("GSV_ENC_MODE");
+    const int mode = em ? atoi(em) : 2;
+#define GSV_ENC_LAUNCH(M)                                                                               \
+    cudaFuncSetAttribute(rc_encode_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    rc_encode_kernel<M><<<c.blk[3], kEncRPW, smem, s>>>(d_runs, d_order, c, d_res)
+    if (mode == 0) {
+        GSV_ENC_LAUNCH(0);
+    } else if (mode == 1) {
+        GSV_ENC_LAUNCH(1);
     } else {
-        cudaFuncSetAttribute(rc_encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_encode_kernel<false><<<c.blk[3], kEncRPW, smem, s>>>(d_runs, d_order, c, d_res);
+        GSV_ENC_LAUNCH(2);
     }
+#undef GSV_ENC_LAUNCH
     if (nplanes) enc_raw_blocks_kernel<<<nplanes < 148 * 8 ? nplanes : 148 * 8, 256, 0, s>>>(
         d_runs, d_res, d_plane_prefix, nruns, nplanes);
 }

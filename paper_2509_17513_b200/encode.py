@@ -16,6 +16,8 @@ from __future__ import annotations
 import math
 import os
 import struct
+import sys
+import time
 import zlib
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -297,7 +299,11 @@ def _gpu_finish(pending: list, codecs: Sequence[int], sess) -> list:
                 _, _, _, bits, _, _, w, h = g.chans[i]
                 runs[k] = _lib.EncodeRun_t(g.planes.data_ptr() + g.offs[i], bodies.data_ptr() + int(boffs[k]),
                                            g.nf, w, h, bits, 0, 0, 0)
+            t0 = time.perf_counter()
             _lib.check(L.gsv_encode_runs(sess.handle, runs, len(items)))
+            if os.environ.get("GSV_DEBUG_ENC_TIMING"):  # dev: range-coder time to stderr
+                print(f"[enc] range-code {len(items)} runs {1e3 * (time.perf_counter() - t0):.1f} ms",
+                      file=sys.stderr)
             h_bodies = bodies.cpu().numpy()
             del bodies
         h_planes = {id(g): g.planes.cpu().numpy() for g in pending} if (0 in codecs or h_bodies is None) else {}
