@@ -309,7 +309,7 @@ __device__ __forceinline__ ProjOut project_one(const SplatIn<DEG>& a, const CamD
 // get ~0 so they sort last), the splat index, and the 48-B record; counts
 // survivors and tracks the depth-bit range of the survivors.
 template <class Loader, int DEG>
-__global__ void __launch_bounds__(128) project_kernel(Loader ld, CamDev cam,
+__global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
                                                       uint64_t* __restrict__ dkey,
                                                       uint32_t* __restrict__ didx,
                                                       SplatRec* __restrict__ rec,

@@ -1,4 +1,7 @@
-# dev diagnostic: marginal frame-parallel cost of a stage = throughput drop when it runs twice
-for d in none composite dsort tsort project; do
-  GSV_DEBUG_DOUBLE=$d timeout 900 python bench.py --no-sweep --no-cpu --no-e2e --steps 3 > gpurun_out/dbl_$d.json 2>/dev/null
+# dev diagnostic: marginal cost of each stage in the frame-parallel steady
+# state -- the stage is launched twice (idempotent stages only), the extra
+# ms per step is its marginal cost
+for st in ${STAGES:-none composite tsort dsort emit project gather fixup lastround}; do
+  GSV_DEBUG_DOUBLE=$st timeout 900 python bench.py --no-sweep --no-cpu --no-e2e --steps 5 2>/dev/null | tail -1 | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$st', d['value'], d['ms_per_step'])"
 done

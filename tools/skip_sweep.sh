@@ -1,4 +1,5 @@
 # dev diagnostic: frame-parallel throughput with stages skipped (images invalid)
-for sk in none composite tsort dsort emit project composite,tsort,dsort,emit; do
-  GSV_DEBUG_SKIP=$sk timeout 900 python bench.py --no-sweep --no-cpu --no-e2e --steps 3 > gpurun_out/skip_$sk.json 2>/dev/null
+for sk in ${SKIPS:-none composite tsort dsort emit project gather fixup}; do
+  GSV_DEBUG_SKIP=$sk timeout 900 python bench.py --no-sweep --no-cpu --no-e2e --steps 3 2>/dev/null | tail -1 | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$sk', d['value'], d['ms_per_step'])"
 done
