@@ -78,8 +78,20 @@ __global__ void __launch_bounds__(256) crc_kernel(const RunDesc* __restrict__ ru
         const uint8_t* p = pr.samples + off;
         uint32_t crc = 0xFFFFFFFFu;
         uint32_t i = 0;
-        const uint32_t head = (uint32_t)((8 - ((uintptr_t)p & 7)) & 7);
+        // 16-B loads (a thread walks its own 1 KiB chunk, so every load
+        // instruction touches 32 separate sectors: use all 16 B of each)
+        const uint32_t head = (uint32_t)((16 - ((uintptr_t)p & 15)) & 15);
         for (; i < head && i < len; i++) crc = T[0][(crc ^ p[i]) & 0xFF] ^ (crc >> 8);
+        for (; i + 16 <= len; i += 16) {
+            const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p + i));
+            uint32_t a = crc ^ w.x, b = w.y;
+            crc = T[7][a & 0xFF] ^ T[6][(a >> 8) & 0xFF] ^ T[5][(a >> 16) & 0xFF] ^ T[4][a >> 24] ^
+                  T[3][b & 0xFF] ^ T[2][(b >> 8) & 0xFF] ^ T[1][(b >> 16) & 0xFF] ^ T[0][b >> 24];
+            a = crc ^ w.z;
+            b = w.w;
+            crc = T[7][a & 0xFF] ^ T[6][(a >> 8) & 0xFF] ^ T[5][(a >> 16) & 0xFF] ^ T[4][a >> 24] ^
+                  T[3][b & 0xFF] ^ T[2][(b >> 8) & 0xFF] ^ T[1][(b >> 16) & 0xFF] ^ T[0][b >> 24];
+        }
         for (; i + 8 <= len; i += 8) {
             const uint2 w = *reinterpret_cast<const uint2*>(p + i);
             const uint32_t a = crc ^ w.x, b = w.y;
