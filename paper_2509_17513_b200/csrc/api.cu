@@ -911,10 +911,16 @@ int gsv_fold_deltas(gsv_session* s, int64_t n, int shdim, double* pos, double* r
     int* bad = nullptr;
     GSV_CUDA(cudaMalloc(&bad, sizeof(int)));
     cudaMemsetAsync(bad, 0, sizeof(int), s->stream);
-    for (int d = 0; d < nd; d++)
-        launch_fold(n, shdim, pos, rot, scl, opac, sh, d_trans[d], d_rot[d], d_scl[d], d_opac[d], d_sh[d],
-                    bad, s->stream);
-    count_launch(nd);
+    std::vector<FoldTab> tab(nd);
+    for (int d = 0; d < nd; d++) tab[d] = FoldTab{d_trans[d], d_rot[d], d_scl[d], d_opac[d], d_sh[d]};
+    DevBuf d_tab;
+    int rc = upload(d_tab, tab, s->stream);
+    if (rc) {
+        cudaFree(bad);
+        return rc;
+    }
+    launch_fold_all(n, shdim, pos, rot, scl, opac, sh, d_tab.as<FoldTab>(), nd, bad, s->stream);  // one pass
+    count_launch(1);
     int h = 0;
     cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
     cudaError_t e = cudaStreamSynchronize(s->stream);

@@ -280,6 +280,15 @@ int ssim_device(const void* a, const void* b, int H, int W, bool f64, double* ou
 int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s);
+struct FoldTab {  // one frame delta (motion.py:58-141), device pointers
+    const double* dt;
+    const double* dq;
+    const double* ds;
+    const double* dop;
+    const double* dsh;
+};
+void launch_fold_all(int64_t n, int shdim, double* pos, double* rot, double* scl, double* opac, double* sh,
+                     const FoldTab* tab, int nd, int* bad, cudaStream_t s);
 void launch_fold(int64_t n, int shdim, double* pos, double* rot, double* scl, double* opac,
                  double* sh, const double* dt, const double* dq, const double* ds,
                  const double* dop, const double* dsh, int* bad, cudaStream_t s);

@@ -528,6 +528,81 @@ __global__ void fold_kernel(int64_t n, int shdim, double* __restrict__ pos, doub
     for (int k = 0; k < shdim; k++) sh[(int64_t)shdim * i + k] = sh[(int64_t)shdim * i + k] + dsh[(int64_t)shdim * i + k];
 }
 
+// All deltas of a reconstruct_frame in one pass: the splat's rigid state
+// (position, rotation, scales, opacity: 11 fp64) stays in registers across
+// the deltas and is read and written once; the SH coefficients are folded
+// 12 at a time (their update is a plain running sum, same order).  HBM
+// traffic per splat: 2 x 184 B of state + 184 B per delta, instead of
+// 3 x 184 B per delta with one launch per delta.
+__global__ void __launch_bounds__(256) fold_all_kernel(int64_t n, int shdim, double* __restrict__ pos,
+                                                       double* __restrict__ rot, double* __restrict__ scl,
+                                                       double* __restrict__ opac, double* __restrict__ sh,
+                                                       const FoldTab* __restrict__ tab, int nd,
+                                                       int* __restrict__ bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p0 = pos[3 * i], p1 = pos[3 * i + 1], p2 = pos[3 * i + 2];
+    double bw = rot[4 * i], bx = rot[4 * i + 1], by = rot[4 * i + 2], bz = rot[4 * i + 3];
+    double s0 = scl[3 * i], s1 = scl[3 * i + 1], s2 = scl[3 * i + 2];
+    double o = opac[i];
+    bool zero = false;
+    for (int d = 0; d < nd; d++) {
+        const FoldTab t = tab[d];
+        const double aw = __ldg(t.dq + 4 * i), ax = __ldg(t.dq + 4 * i + 1), ay = __ldg(t.dq + 4 * i + 2),
+                     az = __ldg(t.dq + 4 * i + 3);
+        const double w = ((aw * bw - ax * bx) - ay * by) - az * bz;
+        const double x = ((aw * bx + ax * bw) + ay * bz) - az * by;
+        const double y = ((aw * by - ax * bz) + ay * bw) + az * bx;
+        const double z = ((aw * bz + ax * by) - ay * bx) + az * bw;
+        const double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
+        zero |= nrm == 0.0;
+        bw = w / nrm;
+        bx = x / nrm;
+        by = y / nrm;
+        bz = z / nrm;
+        p0 = p0 + __ldg(t.dt + 3 * i);
+        p1 = p1 + __ldg(t.dt + 3 * i + 1);
+        p2 = p2 + __ldg(t.dt + 3 * i + 2);
+        s0 = np_max(s0 + __ldg(t.ds + 3 * i), 1e-7);
+        s1 = np_max(s1 + __ldg(t.ds + 3 * i + 1), 1e-7);
+        s2 = np_max(s2 + __ldg(t.ds + 3 * i + 2), 1e-7);
+        o = np_min(np_max(o + __ldg(t.dop + i), 0.0), 1.0);
+    }
+    if (zero) *bad = 1;
+    pos[3 * i] = p0;
+    pos[3 * i + 1] = p1;
+    pos[3 * i + 2] = p2;
+    rot[4 * i] = bw;
+    rot[4 * i + 1] = bx;
+    rot[4 * i + 2] = by;
+    rot[4 * i + 3] = bz;
+    scl[3 * i] = s0;
+    scl[3 * i + 1] = s1;
+    scl[3 * i + 2] = s2;
+    opac[i] = o;
+    double* shi = sh + (int64_t)shdim * i;
+    for (int k0 = 0; k0 < shdim; k0 += 12) {
+        double acc[12];
+#pragma unroll
+        for (int k = 0; k < 12; k++) acc[k] = k0 + k < shdim ? shi[k0 + k] : 0.0;
+        for (int d = 0; d < nd; d++) {
+            const double* dsh = tab[d].dsh + (int64_t)shdim * i + k0;
+#pragma unroll
+            for (int k = 0; k < 12; k++)
+                if (k0 + k < shdim) acc[k] = acc[k] + __ldg(dsh + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 12; k++)
+            if (k0 + k < shdim) shi[k0 + k] = acc[k];
+    }
+}
+
+void launch_fold_all(int64_t n, int shdim, double* pos, double* rot, double* scl, double* opac, double* sh,
+                     const FoldTab* tab, int nd, int* bad, cudaStream_t s) {
+    if (n <= 0 || nd <= 0) return;
+    fold_all_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, shdim, pos, rot, scl, opac, sh, tab, nd, bad);
+}
+
 void launch_fold(int64_t n, int shdim, double* pos, double* rot, double* scl, double* opac,
                  double* sh, const double* dt, const double* dq, const double* ds,
                  const double* dop, const double* dsh, int* bad, cudaStream_t s) {

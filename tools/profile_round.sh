@@ -11,3 +11,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_d
      -o gpurun_out/prof/full_rc_decode python tools/rc_bench.py --planes 3 3 > gpurun_out/prof/full_rc_decode.log 2>&1
 ENC_N=50000 ENC_FRAMES=30 ENC_SKIP_HOST=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_encode -c 1 \
      -o gpurun_out/prof/full_rc_encode python tools/enc_bench.py > gpurun_out/prof/full_rc_encode.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fold -s 1 -c 1 \
+     -o gpurun_out/prof/full_fold python tools/fold_driver.py > gpurun_out/prof/full_fold.log 2>&1
