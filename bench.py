@@ -526,14 +526,14 @@ def stage_bytes(a, blob, stage, st):
     per_frame = {
         # codes in (26 B/splat at SH degree 1), depth key + index + 64-B record out
         "project": 26 * n + 12 * n + 64 * nvis,
-        # 4 passes: read + write (4-B key, 4-B index)
-        "depth_sort": 4 * 2 * 8 * n,
-        # gather (index + record in, record out) and key emission (record in, key out)
-        "key_emit": (4 + 64 + 64) * nvis + 64 * nvis + 8 * k_emit,
+        # 3 passes (24-bit key): read + write (4-B key, 4-B index)
+        "depth_sort": 3 * 2 * 8 * n,
+        # key emission: rank -> index, the record's rect (8 B), the (tile, index) keys out
+        "key_emit": (4 + 8) * nvis + 8 * k_emit,
         # 2 passes over the emitted (tile, rank) keys
         "tile_sort": 2 * 2 * 8 * k_emit,
         "tile_ranges": 0,
-        # per emitted key: rank + 48 B of the record used; the fp32 image out
+        # per emitted key: splat index + 48 B of the record used; the fp32 image out
         "composite": (4 + 48) * k_emit + 12 * npx,
     }
     if stage in per_frame:

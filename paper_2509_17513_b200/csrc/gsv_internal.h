@@ -170,7 +170,6 @@ struct RenderWork {
     uint64_t* dkey[2] = {nullptr, nullptr};  // depth sort keys (ping-pong)
     uint32_t* didx[2] = {nullptr, nullptr};  // splat indices (ping-pong)
     SplatRec* rec = nullptr;                 // by splat index
-    SplatRec* rec_sorted = nullptr;          // by depth rank
     uint32_t* cnt = nullptr;                 // tile count by rank -> exclusive offsets
     // per key
     uint32_t* tkey[2] = {nullptr, nullptr};

@@ -308,6 +308,11 @@ __device__ __forceinline__ ProjOut project_one(const SplatIn<DEG>& a, const CamD
 // One thread per splat.  Writes the depth sort key (fp64 bits; culled splats
 // get ~0 so they sort last), the splat index, and the 48-B record; counts
 // survivors and tracks the depth-bit range of the survivors.
+__device__ __forceinline__ uint32_t rect_tiles(uint32_t rx, uint32_t ry) {
+    const uint32_t x0 = rx & 0xFFFFu, x1 = rx >> 16, y0 = ry & 0xFFFFu, y1 = ry >> 16;
+    return ((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1);
+}
+
 template <class Loader, int DEG>
 __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
                                                       uint64_t* __restrict__ dkey,
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = false;
     uint64_t key = ~0ull;
+    uint32_t ntile = 0;  // (tile, splat) overlaps of this splat's rect (render stats)
     if (i < n) {
         SplatIn<DEG> a;
         typename Loader::template Codes<DEG> codes;
@@ -357,6 +363,7 @@ __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
             r.rx = (uint32_t)o.x0 | ((uint32_t)o.x1 << 16);
             r.ry = (uint32_t)o.y0 | ((uint32_t)o.y1 << 16);
             rec[i] = r;
+            ntile = rect_tiles(r.rx, r.ry);
         }
         if (dbg_rect) {
             dbg_rect[4 * i] = alive ? (int32_t)o.x0 : 0;
@@ -375,10 +382,14 @@ __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
         kmin = min(kmin, (uint64_t)__shfl_xor_sync(0xffffffffu, kmin, off));
         kmax = max(kmax, (uint64_t)__shfl_xor_sync(0xffffffffu, kmax, off));
     }
+    unsigned long long tot = ntile;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
     if ((threadIdx.x & 31) == 0 && m) {
         atomicAdd(ctr + 0, (unsigned long long)__popc(m));
         atomicMin(ctr + 2, (unsigned long long)kmin);
         atomicMax(ctr + 3, (unsigned long long)kmax);
+        atomicAdd(ctr + 10, tot);  // C_TOTK
     }
 }
 
@@ -442,6 +453,7 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = false;
     uint64_t key = ~0ull;
+    uint32_t ntile = 0;
     if (i < n) {
         const double mx = means[2 * i], my = means[2 * i + 1];
         const double A = cov[4 * i], B = cov[4 * i + 1], C = cov[4 * i + 3];
@@ -473,6 +485,7 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
             r.rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             r.ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
             rec[i] = r;
+            ntile = rect_tiles(r.rx, r.ry);
         }
         dkey[i] = key;
         didx[i] = (uint32_t)i;
@@ -484,10 +497,14 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
         kmin = min(kmin, (uint64_t)__shfl_xor_sync(0xffffffffu, kmin, off));
         kmax = max(kmax, (uint64_t)__shfl_xor_sync(0xffffffffu, kmax, off));
     }
+    unsigned long long tot = ntile;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
     if ((threadIdx.x & 31) == 0 && m) {
         atomicAdd(ctr + 0, (unsigned long long)__popc(m));
         atomicMin(ctr + 2, (unsigned long long)kmin);
         atomicMax(ctr + 3, (unsigned long long)kmax);
+        atomicAdd(ctr + 10, tot);  // C_TOTK
     }
 }
 

@@ -168,25 +168,6 @@ __device__ __forceinline__ uint32_t rec_tile_count(const SplatRec& r) {
     return ((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1);
 }
 
-// rank r -> record in rank order
-// (also totals the (tile, splat) overlaps: the tile-key count without early out)
-__global__ void gather_sorted(const SplatRec* __restrict__ rec, SplatRec* __restrict__ rec_sorted,
-                              unsigned long long* __restrict__ ctr, const uint32_t* __restrict__ didx0,
-                              const uint32_t* __restrict__ didx1) {
-    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
-    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
-    const uint32_t* idx = (np & 1) ? didx1 : didx0;
-    unsigned long long tot = 0;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nvis; r += gridDim.x * blockDim.x) {
-        const SplatRec s = rec[idx[r]];
-        rec_sorted[r] = s;
-        tot += rec_tile_count(s);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(ctr + C_TOTK, tot);
-}
-
 // Round [a, b) of the depth ranks: count the not-yet-saturated tiles each
 // splat overlaps, turn the counts into offsets with a single-pass
 // decoupled-look-back scan across CTAs (ticketed CTA order, epoch-tagged
@@ -229,7 +210,8 @@ __device__ __forceinline__ uint32_t mask_count(const uint32_t* m, uint32_t lo, u
 constexpr int kMaskWordsSmem = 2048;  // open-tile masks of up to 65536 tiles live in shared memory
 
 __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
-    const SplatRec* __restrict__ rec_sorted, unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
+    const SplatRec* __restrict__ rec, const uint32_t* __restrict__ didx0, const uint32_t* __restrict__ didx1,
+    unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
     const uint32_t* __restrict__ open_mask, int ntiles, uint32_t* __restrict__ tkey,
     uint32_t* __restrict__ tval, uint64_t cap, int ntx, unsigned long long* __restrict__ status,
     unsigned int* __restrict__ ticket, uint32_t epoch, uint32_t* __restrict__ ghist, int tpasses) {
@@ -268,8 +250,14 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     const uint32_t base = tile * kEmitTile + threadIdx.x;
     uint32_t x0 = 1, x1 = 0, y0 = 1, y1 = 0;  // this thread's splat, tile coordinates (inclusive)
     uint32_t sum = 0;
+    // depth rank -> splat: the sort's index buffer (the pass count decides
+    // which ping-pong half holds it); keys carry the splat index, so the
+    // compositor reads the records where the projection wrote them
+    const uint32_t* order = (reinterpret_cast<const int*>(ctr + C_NPASS)[0] & 1) ? didx1 : didx0;
+    uint32_t sidx = 0;
     if (base < m) {
-        const SplatRec* sr = rec_sorted + a + base;
+        sidx = __ldg(order + a + base);
+        const SplatRec* sr = rec + sidx;
         const uint2 r = make_uint2(__ldg(&sr->rx), __ldg(&sr->ry));
         x0 = (r.x & 0xFFFFu) / kTile;
         x1 = ((r.x >> 16) - 1) / kTile;
@@ -342,7 +330,7 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     // scatter this thread's splat's keys in rank order (open tiles only)
     if (sum) {
         unsigned long long o = s_prefix + excl;
-        const uint32_t r = a + base;
+        const uint32_t r = sidx;
         for (uint32_t ty = y0; ty <= y1; ty++)
             for (uint32_t tx = x0; tx <= x1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
@@ -383,7 +371,6 @@ void work_free(RenderWork* w) {
         free_ptr(w->tval[b]);
     }
     free_ptr(w->rec);
-    free_ptr(w->rec_sorted);
     free_ptr(w->cnt);
     free_ptr(w->range);
     free_ptr(w->state);
@@ -414,10 +401,8 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
             GSV_CUDA(cudaMalloc(&w->didx[b], c * sizeof(uint32_t)));
         }
         free_ptr(w->rec);
-        free_ptr(w->rec_sorted);
-        free_ptr(w->cnt);
+            free_ptr(w->cnt);
         GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
-        GSV_CUDA(cudaMalloc(&w->rec_sorted, c * sizeof(SplatRec)));
         GSV_CUDA(cudaMalloc(&w->cnt, (c + 1) * sizeof(uint32_t)));
         free_ptr(w->status);
         const size_t ns = (size_t)(c / 256 + 4) * sizeof(unsigned long long) + 64;
@@ -594,10 +579,6 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         count_launch(2 + radix_launches(depth_key_bits() / 8, true));
     }
     prof_mark(ST_EMIT, s);
-    const unsigned g = 148 * 4;
-    gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
-    if (dbl & 32) gather_sorted<<<g, 256, 0, s>>>(w->rec, w->rec_sorted, ctr, w->didx[0], w->didx[1]);
-    count_launch(1);
     std::vector<uint32_t> bounds;
     round_bounds(n, &bounds);
     const int tp = tile_passes(ntiles);
@@ -613,7 +594,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                                                                   ntiles, mask);
             count_launch(1);
         }
-        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec_sorted, ctr, a, b, mask, ntiles, w->tkey[0],
+        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, mask, ntiles, w->tkey[0],
                                                       w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
                                                       w->ticket, ++w->epoch, th, tp);
         count_launch(1);
@@ -623,13 +604,13 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         count_launch(radix_launches(tp, true));
         prof_mark(ST_COMPOSITE, s);
         if ((dbl & 1) && j == 0)
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
                                    w->tile_done, cam, true, false, out_rgb, out_rgb8, s);
         if (!(skip & 1))
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
                                    w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
         if ((dbl & 128) && j > 0 && j + 2 == bounds.size())
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec_sorted, w->state,
+            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
                                    w->tile_done, cam, false, true, out_rgb, out_rgb8, s);
         count_launch(1);
     }
