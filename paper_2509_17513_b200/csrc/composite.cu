@@ -134,7 +134,7 @@ __device__ __forceinline__ float ex2f(float x) {
 // (record, column) -- a different fp32 rounding of the same fp64 quantity.
 template <int ROWS, bool PACKED, bool TEFF>
 __global__ void __launch_bounds__(128) composite_strip_kernel(
-    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
@@ -151,8 +151,10 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const uint8_t td = first ? kTileOpen : *flag;
     if (td == kTileSaturated) return;
     const uint32_t K = (uint32_t)*nkeys;
-    const uint32_t start = warp_lower_bound(keys, K, (uint32_t)tile);
-    const uint32_t end = warp_lower_bound(keys, K, (uint32_t)tile + 1);
+    // tile range: from the round-1 binning's offsets, or a search of the
+    // sorted tile keys
+    const uint32_t start = tile_off ? min(__ldg(tile_off + tile), K) : warp_lower_bound(keys, K, (uint32_t)tile);
+    const uint32_t end = tile_off ? min(__ldg(tile_off + tile + 1), K) : warp_lower_bound(keys, K, (uint32_t)tile + 1);
     bool on = true;
     const int tx = on ? tile % ntx : 0, ty = on ? tile / ntx : 0;
     const int px = tx * kTile + (lane & 15);
@@ -381,7 +383,7 @@ int composite_rows() {
     return rows;
 }
 
-void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
+void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, const uint32_t* ranks,
                             const unsigned long long* nkeys, const SplatRec* recs, float4* state,
                             uint8_t* tile_done, const CamDev& cam, bool first, bool last, float* out_rgb,
                             uint8_t* out_rgb8, cudaStream_t s) {
@@ -396,7 +398,7 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
         packed = e ? atoi(e) : 2;
     }
 #define GSV_COMPOSITE(R, P, E)                                                                          \
-    composite_strip_kernel<R, P, E><<<grid, 128, 0, s>>>(keys, ranks, nkeys, recs, state, tile_done, cam.width, \
+    composite_strip_kernel<R, P, E><<<grid, 128, 0, s>>>(keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, \
                                                          cam.height, ntx, ntiles, first, last, cam.bg[0],   \
                                                          cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
     if (packed == 2 && rows == 8) {

@@ -178,6 +178,9 @@ struct RenderWork {
     uint32_t* range = nullptr;               // [tiles][2]
     uint8_t* tile_done = nullptr;            // saturated tiles
     uint32_t* open_mask = nullptr;           // bit per tile: still open (later rounds' emission)
+    uint32_t* r1_bc = nullptr;               // round-1 binning: per (rank block, tile) counts / offsets
+    uint32_t* r1_off = nullptr;              // round-1 binning: tile ranges (ntiles + 1)
+    size_t r1_bc_cap = 0, r1_off_cap = 0;
     float4* state = nullptr;                 // per pixel (C.rgb, T) carried across rounds
     int64_t cap_pix = 0;
     // decoupled look-back scan state of the fused key emission
@@ -257,7 +260,7 @@ void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s);
 // final image of every tile still open (saturated tiles are written when they
 // saturate).
 int composite_rows();  // pixel rows per lane of the compositor (GSV_COMPOSITE_ROWS: 2, 4, 8)
-void launch_composite_round(const uint32_t* keys, const uint32_t* ranks,
+void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, const uint32_t* ranks,
                             const unsigned long long* nkeys, const SplatRec* recs, float4* state,
                             uint8_t* tile_done, const CamDev& cam, bool first, bool last, float* out_rgb,
                             uint8_t* out_rgb8, cudaStream_t s);

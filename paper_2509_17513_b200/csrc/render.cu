@@ -348,6 +348,209 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         if (s_hist[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], s_hist[p][threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------
+// First round without a sort.  Every tile is open in round 1, so the
+// (tile, splat) pairs of ranks [a, b) are binned directly, in rank order
+// inside each tile, by counting: the ranks are cut into blocks of B; (1) per
+// block, the tiles each splat's rect covers are counted in shared memory;
+// (2) per tile, the block counts are turned into exclusive offsets and the
+// tile totals into the tile ranges; (3) per block, ONE warp walks its splats
+// in rank order and places each splat index at its tiles' next slot.  The
+// compositor then reads each tile's range directly (no tile keys, no search).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rect_tiles_of(const SplatRec* __restrict__ rec, uint32_t idx, uint32_t& tx0,
+                                              uint32_t& tx1, uint32_t& ty0, uint32_t& ty1) {
+    const uint32_t rx = __ldg(&rec[idx].rx), ry = __ldg(&rec[idx].ry);
+    tx0 = (rx & 0xFFFFu) / kTile;
+    tx1 = ((rx >> 16) - 1) / kTile;
+    ty0 = (ry & 0xFFFFu) / kTile;
+    ty1 = ((ry >> 16) - 1) / kTile;
+}
+
+__global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restrict__ rec,
+                                                       const uint32_t* __restrict__ didx0,
+                                                       const uint32_t* __restrict__ didx1,
+                                                       const unsigned long long* __restrict__ ctr, uint32_t a,
+                                                       uint32_t b, uint32_t B, int ntx, int ntiles,
+                                                       uint32_t* __restrict__ bc) {
+    extern __shared__ uint32_t s_cnt[];
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
+    __syncthreads();
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const uint32_t hi = min(b, nvis);
+    const uint32_t* order = (reinterpret_cast<const int*>(ctr + C_NPASS)[0] & 1) ? didx1 : didx0;
+    const uint32_t r0 = a + blockIdx.x * B, r1 = min(r0 + B, hi);
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        uint32_t tx0, tx1, ty0, ty1;
+        rect_tiles_of(rec, __ldg(order + r), tx0, tx1, ty0, ty1);
+        for (uint32_t ty = ty0; ty <= ty1; ty++)
+            for (uint32_t tx = tx0; tx <= tx1; tx++) atomicAdd(&s_cnt[ty * (uint32_t)ntx + tx], 1u);
+    }
+    __syncthreads();
+    uint32_t* row = bc + (size_t)blockIdx.x * ntiles;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) row[t] = s_cnt[t];
+}
+
+// per tile: block counts -> exclusive offsets inside the tile (in place),
+// tile totals -> off[t].  A CTA takes 32 tiles (one per lane: coalesced
+// 128-B rows) and all blocks, 32 consecutive blocks per warp; the loads of
+// a warp's 32 blocks are independent (all in flight at once)
+__global__ void __launch_bounds__(256) r1_scan_blocks_kernel(uint32_t* __restrict__ bc, int nblk, int ntiles,
+                                                             uint32_t* __restrict__ off) {
+    __shared__ uint32_t s_tot[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const int k0 = warp * 32;
+    uint32_t v[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) v[k] = (t < ntiles && k0 + k < nblk) ? bc[(size_t)(k0 + k) * ntiles + t] : 0u;
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+        const uint32_t x = v[k];
+        v[k] = run;
+        run += x;
+    }
+    s_tot[warp][lane] = run;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        base += w < warp ? s_tot[w][lane] : 0u;
+        tot += s_tot[w][lane];
+    }
+    if (t < ntiles) {
+#pragma unroll
+        for (int k = 0; k < 32; k++)
+            if (k0 + k < nblk) bc[(size_t)(k0 + k) * ntiles + t] = base + v[k];
+        if (warp == 0) off[t] = tot;
+    }
+}
+
+// exclusive scan of the tile totals (one CTA), key counters as the emission
+// would set them (capacity check and re-render on overflow)
+__global__ void __launch_bounds__(1024) r1_scan_tiles_kernel(uint32_t* __restrict__ off, int ntiles,
+                                                             unsigned long long* __restrict__ ctr, uint64_t cap) {
+    __shared__ uint32_t s_w[32];
+    const int per = (ntiles + 1023) / 1024;
+    const int t0 = threadIdx.x * per;
+    uint32_t sum = 0;
+    for (int i = 0; i < per; i++)
+        if (t0 + i < ntiles) sum += off[t0 + i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        s_w[lane] = v;
+    }
+    __syncthreads();
+    uint32_t run = (warp ? s_w[warp - 1] : 0u) + x - sum;
+    for (int i = 0; i < per; i++)
+        if (t0 + i < ntiles) {
+            const uint32_t v = off[t0 + i];
+            off[t0 + i] = run;
+            run += v;
+        }
+    if (threadIdx.x == 1023) {
+        const unsigned long long K = s_w[31];
+        off[ntiles] = (uint32_t)K;
+        ctr[C_NKEYS] = K;
+        ctr[C_KCLAMP] = K < cap ? K : cap;
+        if (K > cap) ctr[C_OVF] = K;
+        atomicMax(ctr + C_MAXK, K);
+        ctr[C_EMITK] += K;
+    }
+}
+
+// one warp per block of ranks: splats in rank order, each one's tiles
+// spread over the lanes; a tile's next slot lives in shared memory
+__global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restrict__ rec,
+                                                      const uint32_t* __restrict__ didx0,
+                                                      const uint32_t* __restrict__ didx1,
+                                                      const unsigned long long* __restrict__ ctr, uint32_t a,
+                                                      uint32_t b, uint32_t B, int ntx, int ntiles,
+                                                      const uint32_t* __restrict__ bc,
+                                                      const uint32_t* __restrict__ off, uint32_t* __restrict__ val,
+                                                      uint64_t cap) {
+    extern __shared__ uint32_t s_next[];
+    const uint32_t* row = bc + (size_t)blockIdx.x * ntiles;
+    for (int t0 = threadIdx.x; t0 < ntiles; t0 += 4 * blockDim.x) {  // 4 independent pairs in flight
+        uint32_t o4[4], r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int t = t0 + u * blockDim.x;
+            o4[u] = t < ntiles ? __ldg(off + t) : 0u;
+            r4[u] = t < ntiles ? __ldg(row + t) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (t0 + u * (int)blockDim.x < ntiles) s_next[t0 + u * blockDim.x] = o4[u] + r4[u];
+    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;  // the placement itself is one warp, in rank order
+    const uint32_t nvis = (uint32_t)ctr[C_NVIS];
+    const uint32_t hi = min(b, nvis);
+    const uint32_t* order = (reinterpret_cast<const int*>(ctr + C_NPASS)[0] & 1) ? didx1 : didx0;
+    const uint32_t r0 = a + blockIdx.x * B, r1 = min(r0 + B, hi);
+    const int lane = threadIdx.x;
+    // 32 splats' rects at a time (the next 32 loaded while these are
+    // placed), then one splat after the other
+    uint32_t nidx = 0, nrx = 0, nry = 0;
+    auto fetch = [&](uint32_t base) {
+        const uint32_t rr = base + lane;
+        nidx = 0;
+        nrx = nry = 0;
+        if (rr < r1) {
+            nidx = __ldg(order + rr);
+            nrx = __ldg(&rec[nidx].rx);
+            nry = __ldg(&rec[nidx].ry);
+        }
+    };
+    if (r0 < r1) fetch(r0);
+    for (uint32_t base = r0; base < r1; base += 32) {
+        const uint32_t idx = nidx, rx = nrx, ry = nry;
+        if (base + 32 < r1) fetch(base + 32);
+        // per lane, for its own splat (off the sequential chain): first tile,
+        // rect width and area in tiles, and the multiplier of k / w
+        uint32_t t0 = 0, w = 1, area = 0, mw = 0;
+        if (base + lane < r1) {
+            const uint32_t tx0 = (rx & 0xFFFFu) / kTile, tx1 = ((rx >> 16) - 1) / kTile;
+            const uint32_t ty0 = (ry & 0xFFFFu) / kTile, ty1 = ((ry >> 16) - 1) / kTile;
+            t0 = ty0 * (uint32_t)ntx + tx0;
+            w = tx1 - tx0 + 1;
+            area = w * (ty1 - ty0 + 1);
+            // k / w as one multiply-high, exact for k * w < 2^32 (w = 1:
+            // the multiplier would be 2^32, handled apart)
+            mw = w > 1 ? 0xFFFFFFFFu / w + 1u : 0u;
+        }
+        const int cnt = (int)min(32u, r1 - base);
+        for (int q = 0; q < cnt; q++) {
+            const uint32_t sidx = __shfl_sync(0xffffffffu, idx, q), qt0 = __shfl_sync(0xffffffffu, t0, q);
+            const uint32_t qw = __shfl_sync(0xffffffffu, w, q), qa = __shfl_sync(0xffffffffu, area, q);
+            const uint32_t qm = __shfl_sync(0xffffffffu, mw, q);
+            for (uint32_t k = lane; k < qa; k += 32) {
+                const uint32_t dy = qw > 1 ? __umulhi(k, qm) : k, dx = k - dy * qw;
+                const uint32_t t = qt0 + dy * (uint32_t)ntx + dx;
+                const uint32_t pos = s_next[t]++;
+                if (pos < cap) val[pos] = sidx;
+            }
+            __syncwarp();
+        }
+    }
+}
+
 __global__ void tile_ranges(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ ctr,
                             uint32_t* __restrict__ range) {
     const uint32_t K = (uint32_t)ctr[C_KCLAMP];
@@ -376,6 +579,8 @@ void work_free(RenderWork* w) {
     free_ptr(w->state);
     free_ptr(w->tile_done);
     free_ptr(w->open_mask);
+    free_ptr(w->r1_bc);
+    free_ptr(w->r1_off);
     free_ptr(w->status);
     free_ptr(w->sort_ghist);
     free_ptr(w->sort_status);
@@ -464,6 +669,33 @@ static uint32_t open_word(int rows) {
 }
 
 static unsigned prep_grid(int64_t n) { return (unsigned)std::min<int64_t>((n + 1023) / 1024, 148 * 2); }
+
+// round-1 counting placement (dev toggle GSV_R1_BIN=0: emit + tile sort as in later rounds)
+static bool r1_binning() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GSV_R1_BIN");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+static int r1_reserve(RenderWork* w, size_t bc_words, size_t off_words) {
+    if (bc_words > w->r1_bc_cap) {
+        free_ptr(w->r1_bc);
+        w->r1_bc = nullptr;
+        const size_t c = std::max(bc_words, w->r1_bc_cap * 5 / 4);
+        GSV_CUDA(cudaMalloc(&w->r1_bc, c * 4));
+        w->r1_bc_cap = c;
+    }
+    if (off_words > w->r1_off_cap) {
+        free_ptr(w->r1_off);
+        w->r1_off = nullptr;
+        GSV_CUDA(cudaMalloc(&w->r1_off, off_words * 4));
+        w->r1_off_cap = off_words;
+    }
+    return GSV_OK;
+}
 
 static int tile_passes(int ntiles) {
     int bits = 0;
@@ -594,24 +826,56 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                                                                   ntiles, mask);
             count_launch(1);
         }
-        if (!(skip & 8)) round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, mask, ntiles, w->tkey[0],
-                                                      w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
-                                                      w->ticket, ++w->epoch, th, tp);
-        count_launch(1);
-        prof_mark(ST_TSORT, s);
-        if (!(skip & 2)) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
-        if (dbl & 2) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
-        count_launch(radix_launches(tp, true));
+        const bool bin = j == 0 && r1_binning();
+        const uint32_t* keys = w->tkey[tp & 1];
+        const uint32_t* vals = w->tval[tp & 1];
+        const uint32_t* toff = nullptr;
+        if (bin) {
+            // round 1: every tile open -> counting placement instead of emit + sort
+            const uint32_t span = b - a;
+            uint32_t B = std::max<uint32_t>(128u, (span + 255u) / 256u);
+            B = (B + 31u) & ~31u;
+            const uint32_t nblk = std::max<uint32_t>(1u, (span + B - 1) / B);
+            int rc = r1_reserve(w, (size_t)nblk * ntiles, (size_t)ntiles + 1);
+            if (rc) return rc;
+            const size_t sm = (size_t)ntiles * 4;
+            static size_t sm_set = 48 * 1024;
+            if (sm > sm_set) {
+                cudaFuncSetAttribute(r1_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                cudaFuncSetAttribute(r1_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                sm_set = sm;
+            }
+            r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc);
+            r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 256, 0, s>>>(w->r1_bc, (int)nblk, ntiles, w->r1_off);
+            r1_scan_tiles_kernel<<<1, 1024, 0, s>>>(w->r1_off, ntiles, ctr, (uint64_t)w->cap_k);
+            prof_mark(ST_TSORT, s);
+            r1_place_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc,
+                                                 w->r1_off, w->tval[0], (uint64_t)w->cap_k);
+            count_launch(4);
+            keys = nullptr;
+            vals = w->tval[0];
+            toff = w->r1_off;
+        } else {
+            if (!(skip & 8))
+                round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, mask, ntiles,
+                                                           w->tkey[0], w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
+                                                           w->ticket, ++w->epoch, th, tp);
+            count_launch(1);
+            prof_mark(ST_TSORT, s);
+            if (!(skip & 2)) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
+            if (dbl & 2) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
+            count_launch(radix_launches(tp, true));
+        }
         prof_mark(ST_COMPOSITE, s);
         if ((dbl & 1) && j == 0)
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
-                                   w->tile_done, cam, true, false, out_rgb, out_rgb8, s);
+            launch_composite_round(keys, toff, vals, ctr + C_KCLAMP, w->rec, w->state, w->tile_done, cam, true, false,
+                                   out_rgb, out_rgb8, s);
         if (!(skip & 1))
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
-                                   w->tile_done, cam, j == 0, j + 2 == bounds.size(), out_rgb, out_rgb8, s);
+            launch_composite_round(keys, toff, vals, ctr + C_KCLAMP, w->rec, w->state, w->tile_done, cam, j == 0,
+                                   j + 2 == bounds.size(), out_rgb, out_rgb8, s);
         if ((dbl & 128) && j > 0 && j + 2 == bounds.size())
-            launch_composite_round(w->tkey[tp & 1], w->tval[tp & 1], ctr + C_KCLAMP, w->rec, w->state,
-                                   w->tile_done, cam, false, true, out_rgb, out_rgb8, s);
+            launch_composite_round(keys, toff, vals, ctr + C_KCLAMP, w->rec, w->state, w->tile_done, cam, false, true,
+                                   out_rgb, out_rgb8, s);
         count_launch(1);
     }
     prof_mark(ST_COUNT, s);
