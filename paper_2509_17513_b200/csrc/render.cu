@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restric
                                                        const uint32_t* __restrict__ didx1,
                                                        const unsigned long long* __restrict__ ctr, uint32_t a,
                                                        uint32_t b, uint32_t B, int ntx, int ntiles,
-                                                       uint32_t* __restrict__ bc) {
+                                                       const uint32_t* __restrict__ mask, uint32_t* __restrict__ bc) {
     extern __shared__ uint32_t s_cnt[];
     for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
     __syncthreads();
@@ -384,7 +384,10 @@ __global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restric
         uint32_t tx0, tx1, ty0, ty1;
         rect_tiles_of(rec, __ldg(order + r), tx0, tx1, ty0, ty1);
         for (uint32_t ty = ty0; ty <= ty1; ty++)
-            for (uint32_t tx = tx0; tx <= tx1; tx++) atomicAdd(&s_cnt[ty * (uint32_t)ntx + tx], 1u);
+            for (uint32_t tx = tx0; tx <= tx1; tx++) {
+                const uint32_t t = ty * (uint32_t)ntx + tx;
+                if (!mask || ((__ldg(mask + (t >> 5)) >> (t & 31)) & 1u)) atomicAdd(&s_cnt[t], 1u);
+            }
     }
     __syncthreads();
     uint32_t* row = bc + (size_t)blockIdx.x * ntiles;
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restric
                                                       uint32_t b, uint32_t B, int ntx, int ntiles,
                                                       const uint32_t* __restrict__ bc,
                                                       const uint32_t* __restrict__ off, uint32_t* __restrict__ val,
-                                                      uint64_t cap) {
+                                                      uint64_t cap, const uint32_t* __restrict__ mask) {
     extern __shared__ uint32_t s_next[];
     const uint32_t* row = bc + (size_t)blockIdx.x * ntiles;
     for (int t0 = threadIdx.x; t0 < ntiles; t0 += 4 * blockDim.x) {  // 4 independent pairs in flight
@@ -534,15 +537,22 @@ __global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restric
             // k / w as one multiply-high, exact for k * w < 2^32 (w = 1:
             // the multiplier would be 2^32, handled apart)
             mw = w > 1 ? 0xFFFFFFFFu / w + 1u : 0u;
+            if (mask) {  // later rounds: splats whose tiles are all closed place nothing
+                uint32_t open = 0;
+                for (uint32_t ty = ty0; ty <= ty1 && !open; ty++)
+                    open = mask_count(mask, ty * ntx + tx0, ty * ntx + tx1);
+                if (!open) area = 0;
+            }
         }
-        const int cnt = (int)min(32u, r1 - base);
-        for (int q = 0; q < cnt; q++) {
+        for (uint32_t todo = __ballot_sync(0xffffffffu, area != 0); todo; todo &= todo - 1) {
+            const int q = __ffs(todo) - 1;
             const uint32_t sidx = __shfl_sync(0xffffffffu, idx, q), qt0 = __shfl_sync(0xffffffffu, t0, q);
             const uint32_t qw = __shfl_sync(0xffffffffu, w, q), qa = __shfl_sync(0xffffffffu, area, q);
             const uint32_t qm = __shfl_sync(0xffffffffu, mw, q);
             for (uint32_t k = lane; k < qa; k += 32) {
                 const uint32_t dy = qw > 1 ? __umulhi(k, qm) : k, dx = k - dy * qw;
                 const uint32_t t = qt0 + dy * (uint32_t)ntx + dx;
+                if (mask && !((__ldg(mask + (t >> 5)) >> (t & 31)) & 1u)) continue;
                 const uint32_t pos = s_next[t]++;
                 if (pos < cap) val[pos] = sidx;
             }
@@ -676,6 +686,18 @@ static bool r1_binning() {
     if (v < 0) {
         const char* e = getenv("GSV_R1_BIN");
         v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+// later rounds binned the same way, open tiles only (dev toggle GSV_R2_BIN=1;
+// measured 7% slower than emit + sort: round 2's ~270k splats mostly place
+// nothing, and the sequential warp still walks them)
+static bool later_binning() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GSV_R2_BIN");
+        v = e ? atoi(e) : 0;
     }
     return v != 0;
 }
@@ -826,7 +848,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                                                                   ntiles, mask);
             count_launch(1);
         }
-        const bool bin = j == 0 && r1_binning();
+        const bool bin = r1_binning() && (j == 0 || later_binning());
         const uint32_t* keys = w->tkey[tp & 1];
         const uint32_t* vals = w->tval[tp & 1];
         const uint32_t* toff = nullptr;
@@ -845,12 +867,13 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                 cudaFuncSetAttribute(r1_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 sm_set = sm;
             }
-            r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc);
+            r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, mask,
+                                                  w->r1_bc);
             r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 256, 0, s>>>(w->r1_bc, (int)nblk, ntiles, w->r1_off);
             r1_scan_tiles_kernel<<<1, 1024, 0, s>>>(w->r1_off, ntiles, ctr, (uint64_t)w->cap_k);
             prof_mark(ST_TSORT, s);
             r1_place_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc,
-                                                 w->r1_off, w->tval[0], (uint64_t)w->cap_k);
+                                                 w->r1_off, w->tval[0], (uint64_t)w->cap_k, mask);
             count_launch(4);
             keys = nullptr;
             vals = w->tval[0];
