@@ -132,8 +132,8 @@ __device__ __forceinline__ float ex2f(float x) {
 // pixel), power clamp, 0.99 alpha cap, alpha <= 0 skip, fp32, fixed order.
 // The quadratic form is evaluated as A + dy (B + C dy) with A, B per
 // (record, column) -- a different fp32 rounding of the same fp64 quantity.
-template <int ROWS, bool PACKED, bool TEFF>
-__global__ void __launch_bounds__(128) composite_strip_kernel(
+template <int ROWS, bool PACKED, bool TEFF, bool RANGES>
+__global__ void __launch_bounds__(128, 5) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
@@ -153,8 +153,14 @@ __global__ void __launch_bounds__(128) composite_strip_kernel(
     const uint32_t K = (uint32_t)*nkeys;
     // tile range: from the round-1 binning's offsets, or a search of the
     // sorted tile keys
-    const uint32_t start = tile_off ? min(__ldg(tile_off + tile), K) : warp_lower_bound(keys, K, (uint32_t)tile);
-    const uint32_t end = tile_off ? min(__ldg(tile_off + tile + 1), K) : warp_lower_bound(keys, K, (uint32_t)tile + 1);
+    uint32_t start, end;
+    if constexpr (RANGES) {
+        start = min(__ldg(tile_off + tile), K);
+        end = min(__ldg(tile_off + tile + 1), K);
+    } else {
+        start = warp_lower_bound(keys, K, (uint32_t)tile);
+        end = warp_lower_bound(keys, K, (uint32_t)tile + 1);
+    }
     bool on = true;
     const int tx = on ? tile % ntx : 0, ty = on ? tile / ntx : 0;
     const int px = tx * kTile + (lane & 15);
@@ -398,9 +404,16 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
         packed = e ? atoi(e) : 2;
     }
 #define GSV_COMPOSITE(R, P, E)                                                                          \
-    composite_strip_kernel<R, P, E><<<grid, 128, 0, s>>>(keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, \
-                                                         cam.height, ntx, ntiles, first, last, cam.bg[0],   \
-                                                         cam.bg[1], cam.bg[2], out_rgb, out_rgb8)
+    do {                                                                                                \
+        if (tile_off)                                                                                   \
+            composite_strip_kernel<R, P, E, true><<<grid, 128, 0, s>>>(                                 \
+                keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
+                last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
+        else                                                                                            \
+            composite_strip_kernel<R, P, E, false><<<grid, 128, 0, s>>>(                                \
+                keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
+                last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
+    } while (0)
     if (packed == 2 && rows == 8) {
         GSV_COMPOSITE(8, true, true);
     } else if (packed) {
