@@ -456,26 +456,26 @@ def timed_e2e_pipelined(a, gsvb, sess, blob, cs, steps, warmup, dist):
     pool = ThreadPoolExecutor(max_workers=nw)
 
     import threading
-    first_open = [threading.Event() for _ in range(nw)]
+    opened = [threading.Event() for _ in range(len(info.groups))]
 
     def worker(w, verify):
         # host thread w drives session w over groups w, w+nw, ... (the C ABI
-        # releases the GIL); thread w starts once thread w-1's first group is
-        # open, so the uploads are staggered (one at a time at full PCIe rate)
-        # instead of bunching up while no frame renders
+        # releases the GIL); group g is opened only after group g-1 is open,
+        # so the uploads go one at a time at full PCIe rate, in group order,
+        # while the other threads render and read back
         torch.cuda.set_device(sess.device)
-        if w > 0:
-            first_open[w - 1].wait()
         for gi in range(w, len(info.groups), nw):
             g = info.groups[gi]
+            if gi > 0:
+                opened[gi - 1].wait()
             v = gsvb.DeviceVideo(host, a.k, session=sessions[w], groups=(gi, gi + 1), info=info)
-            first_open[w].set()
+            opened[gi].set()
             hf = [pinned[starts[gi] + i] for i in range(g.frame_count)]
             v.render_batch(list(range(g.frame_count)), cs, host_u8=hf, streams=a.streams, verify=verify)
             v.close()
 
     def one(verify=False):
-        for e in first_open:
+        for e in opened:
             e.clear()
         for f in [pool.submit(worker, w, verify) for w in range(nw)]:
             f.result()
