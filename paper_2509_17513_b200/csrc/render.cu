@@ -398,9 +398,10 @@ __global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restric
 // tile totals -> off[t].  A CTA takes 32 tiles (one per lane: coalesced
 // 128-B rows) and all blocks, 32 consecutive blocks per warp; the loads of
 // a warp's 32 blocks are independent (all in flight at once)
-__global__ void __launch_bounds__(256) r1_scan_blocks_kernel(uint32_t* __restrict__ bc, int nblk, int ntiles,
+__global__ void __launch_bounds__(512) r1_scan_blocks_kernel(uint32_t* __restrict__ bc, int nblk, int ntiles,
                                                              uint32_t* __restrict__ off) {
-    __shared__ uint32_t s_tot[8][32];
+    __shared__ uint32_t s_tot[16][32];
+    const int nw = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 32 + lane;
     const int k0 = warp * 32;
@@ -417,8 +418,7 @@ __global__ void __launch_bounds__(256) r1_scan_blocks_kernel(uint32_t* __restric
     s_tot[warp][lane] = run;
     __syncthreads();
     uint32_t base = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < 8; w++) {
+    for (int w = 0; w < nw; w++) {
         base += w < warp ? s_tot[w][lane] : 0u;
         tot += s_tot[w][lane];
     }
@@ -702,6 +702,16 @@ static bool later_binning() {
     return v != 0;
 }
 
+static uint32_t r1_block() {  // dev knob GSV_R1_BLOCK: minimum ranks per block (64, 32 measured 7% slower)
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("GSV_R1_BLOCK");
+        v = e ? atoi(e) : 128;
+        if (v < 32) v = 32;
+    }
+    return (uint32_t)v;
+}
+
 static int r1_reserve(RenderWork* w, size_t bc_words, size_t off_words) {
     if (bc_words > w->r1_bc_cap) {
         free_ptr(w->r1_bc);
@@ -855,7 +865,9 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
         if (bin) {
             // round 1: every tile open -> counting placement instead of emit + sort
             const uint32_t span = b - a;
-            uint32_t B = std::max<uint32_t>(128u, (span + 255u) / 256u);
+            // rank blocks (at most 512): the placement walks a block
+            // sequentially, the count matrix grows with the block count
+            uint32_t B = std::max<uint32_t>(r1_block(), (span + 511u) / 512u);
             B = (B + 31u) & ~31u;
             const uint32_t nblk = std::max<uint32_t>(1u, (span + B - 1) / B);
             int rc = r1_reserve(w, (size_t)nblk * ntiles, (size_t)ntiles + 1);
@@ -869,7 +881,8 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             }
             r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, mask,
                                                   w->r1_bc);
-            r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 256, 0, s>>>(w->r1_bc, (int)nblk, ntiles, w->r1_off);
+            r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 32 * ((nblk + 31) / 32), 0, s>>>(w->r1_bc, (int)nblk, ntiles,
+                                                                                          w->r1_off);
             r1_scan_tiles_kernel<<<1, 1024, 0, s>>>(w->r1_off, ntiles, ctr, (uint64_t)w->cap_k);
             prof_mark(ST_TSORT, s);
             r1_place_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc,
