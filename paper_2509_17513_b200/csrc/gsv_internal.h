@@ -170,12 +170,10 @@ struct RenderWork {
     uint64_t* dkey[2] = {nullptr, nullptr};  // depth sort keys (ping-pong)
     uint32_t* didx[2] = {nullptr, nullptr};  // splat indices (ping-pong)
     SplatRec* rec = nullptr;                 // by splat index
-    uint32_t* cnt = nullptr;                 // tile count by rank -> exclusive offsets
     // per key
     uint32_t* tkey[2] = {nullptr, nullptr};
     uint32_t* tval[2] = {nullptr, nullptr};
     // per tile / per pixel
-    uint32_t* range = nullptr;               // [tiles][2]
     uint8_t* tile_done = nullptr;            // saturated tiles
     uint32_t* open_mask = nullptr;           // bit per tile: still open (later rounds' emission)
     uint32_t* r1_bc = nullptr;               // round-1 binning: per (rank block, tile) counts / offsets

@@ -561,15 +561,6 @@ __global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restric
     }
 }
 
-__global__ void tile_ranges(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ ctr,
-                            uint32_t* __restrict__ range) {
-    const uint32_t K = (uint32_t)ctr[C_KCLAMP];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
-        const uint32_t t = key[i];
-        if (i == 0 || key[i - 1] != t) range[2 * t] = i;
-        if (i == K - 1 || key[i + 1] != t) range[2 * t + 1] = i + 1;
-    }
-}
 
 // ---------------------------------------------------------------------------
 static void free_ptr(void* p) {
@@ -584,8 +575,6 @@ void work_free(RenderWork* w) {
         free_ptr(w->tval[b]);
     }
     free_ptr(w->rec);
-    free_ptr(w->cnt);
-    free_ptr(w->range);
     free_ptr(w->state);
     free_ptr(w->tile_done);
     free_ptr(w->open_mask);
@@ -616,9 +605,7 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
             GSV_CUDA(cudaMalloc(&w->didx[b], c * sizeof(uint32_t)));
         }
         free_ptr(w->rec);
-            free_ptr(w->cnt);
         GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
-        GSV_CUDA(cudaMalloc(&w->cnt, (c + 1) * sizeof(uint32_t)));
         free_ptr(w->status);
         const size_t ns = (size_t)(c / 256 + 4) * sizeof(unsigned long long) + 64;
         GSV_CUDA(cudaMalloc(&w->status, ns));
@@ -638,10 +625,8 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         w->cap_k = c;
     }
     if (tiles > w->cap_tiles) {
-        free_ptr(w->range);
         free_ptr(w->tile_done);
         free_ptr(w->open_mask);
-        GSV_CUDA(cudaMalloc(&w->range, (size_t)tiles * 2 * sizeof(uint32_t)));
         GSV_CUDA(cudaMalloc(&w->tile_done, (size_t)tiles * 4));
         GSV_CUDA(cudaMalloc(&w->open_mask, ((size_t)tiles + 31) / 32 * 4 + 4));
         w->cap_tiles = tiles;
