@@ -3,7 +3,7 @@
 mkdir -p gpurun_out/prof
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_codec0.csv python tools/ncu_driver.py 0 > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_codec1.csv python tools/ncu_driver.py 1 > /dev/null 2>&1
-for k in composite_strip radix_onesweep round_emit_fused project_kernel gather_sorted depth_tie_fixup crc_kernel; do
+for k in composite_strip radix_onesweep round_emit_fused project_kernel r1_place r1_count depth_tie_fixup crc_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 2 \
      -o gpurun_out/prof/full_$k python tools/ncu_driver.py 0 > gpurun_out/prof/full_$k.log 2>&1
 done
