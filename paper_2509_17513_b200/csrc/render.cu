@@ -348,6 +348,18 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
         if (s_hist[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], s_hist[p][threadIdx.x]);
 }
 
+// sorted tile keys -> tile range offsets off[t] = first key index >= t
+// (t = 0..ntiles): key i fills the tiles in (key[i-1], key[i]]
+__global__ void keys_to_off_kernel(const uint32_t* __restrict__ key, const unsigned long long* __restrict__ ctr,
+                                   int ntiles, uint32_t* __restrict__ off) {
+    const uint32_t K = (uint32_t)ctr[C_KCLAMP];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= K; i += gridDim.x * blockDim.x) {
+        const uint32_t lo = i == 0 ? 0u : __ldg(key + i - 1) + 1u;
+        const uint32_t hi = i == K ? (uint32_t)ntiles : __ldg(key + i);
+        for (uint32_t t = lo; t <= hi; t++) off[t] = i;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // First round without a sort.  Every tile is open in round 1, so the
 // (tile, splat) pairs of ranks [a, b) are binned directly, in rank order
@@ -697,6 +709,15 @@ static uint32_t r1_block() {  // dev knob GSV_R1_BLOCK: minimum ranks per block 
     return (uint32_t)v;
 }
 
+static bool later_ranges() {  // dev toggle GSV_R2_RANGES
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GSV_R2_RANGES");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 static int r1_reserve(RenderWork* w, size_t bc_words, size_t off_words) {
     if (bc_words > w->r1_bc_cap) {
         free_ptr(w->r1_bc);
@@ -886,6 +907,13 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             if (!(skip & 2)) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
             if (dbl & 2) radix_sort<uint32_t>(w->tkey, w->tval, ctr + C_KCLAMP, w->cap_k, tp, nullptr, th, sc, s);
             count_launch(radix_launches(tp, true));
+            if (later_ranges()) {  // tile ranges for the compositor instead of a key search per tile
+                int rc = r1_reserve(w, 1, (size_t)ntiles + 1);
+                if (rc) return rc;
+                keys_to_off_kernel<<<148 * 2, 256, 0, s>>>(w->tkey[tp & 1], ctr, ntiles, w->r1_off);
+                count_launch(1);
+                toff = w->r1_off;
+            }
         }
         prof_mark(ST_COMPOSITE, s);
         if ((dbl & 1) && j == 0)
