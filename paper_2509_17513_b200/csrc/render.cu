@@ -447,11 +447,17 @@ __global__ void __launch_bounds__(512) r1_scan_blocks_kernel(uint32_t* __restric
 __global__ void __launch_bounds__(1024) r1_scan_tiles_kernel(uint32_t* __restrict__ off, int ntiles,
                                                              unsigned long long* __restrict__ ctr, uint64_t cap) {
     __shared__ uint32_t s_w[32];
+    // up to 32 tiles per thread (32768 tiles: 4K is 32400), loaded at once
+    constexpr int kPer = 32;
     const int per = (ntiles + 1023) / 1024;
     const int t0 = threadIdx.x * per;
+    uint32_t v[kPer];
     uint32_t sum = 0;
-    for (int i = 0; i < per; i++)
-        if (t0 + i < ntiles) sum += off[t0 + i];
+#pragma unroll
+    for (int i = 0; i < kPer; i++) {
+        v[i] = (i < per && t0 + i < ntiles) ? off[t0 + i] : 0u;
+        sum += v[i];
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = sum;
 #pragma unroll
@@ -472,11 +478,11 @@ __global__ void __launch_bounds__(1024) r1_scan_tiles_kernel(uint32_t* __restric
     }
     __syncthreads();
     uint32_t run = (warp ? s_w[warp - 1] : 0u) + x - sum;
-    for (int i = 0; i < per; i++)
-        if (t0 + i < ntiles) {
-            const uint32_t v = off[t0 + i];
+#pragma unroll
+    for (int i = 0; i < kPer; i++)
+        if (i < per && t0 + i < ntiles) {
             off[t0 + i] = run;
-            run += v;
+            run += v[i];
         }
     if (threadIdx.x == 1023) {
         const unsigned long long K = s_w[31];
@@ -864,7 +870,9 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
                                                                   ntiles, mask);
             count_launch(1);
         }
-        const bool bin = r1_binning() && (j == 0 || later_binning());
+        // (binning needs the tile counters in shared memory and the tile scan
+        // covers 32768 tiles: up to 4K frames; larger frames sort)
+        const bool bin = r1_binning() && ntiles <= 32768 && (j == 0 || later_binning());
         const uint32_t* keys = w->tkey[tp & 1];
         const uint32_t* vals = w->tval[tp & 1];
         const uint32_t* toff = nullptr;
