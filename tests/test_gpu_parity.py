@@ -337,3 +337,40 @@ def test_render_edge_cases(gsvb, case):
     assert np.max(np.abs(img - ref)) <= MAX_ABS, case
     if case == "behind_camera":
         assert np.array_equal(img, np.tile(np.asarray(cam.background, np.float64), (H, W, 1)).astype(np.float32))
+
+
+_PATHS_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import paper_2509_17513_b200 as g
+from golden_util import camera, container
+out = []
+for name in ('s1_rc', 'c1mini_rc'):
+    data = container(name)
+    with g.DeviceVideo(data, None) as v:
+        for which in ('axis', 'oblique'):
+            cam = camera(name, which)
+            for t in (0, v.frame_count - 1):
+                out.append(v.render(t, cam).cpu().numpy())
+np.save(sys.argv[2], np.stack([o.ravel() for o in out]) if len({o.size for o in out}) == 1
+        else np.concatenate([o.ravel() for o in out]))
+"""
+
+
+def test_binning_and_sort_paths_render_identically(tmp_path):
+    """The round-1 counting placement and the round-2 tile ranges against the
+    emit + sort + key-search path they replace (GSV_R1_BIN=0 GSV_R2_RANGES=0,
+    also the path of frames above 32768 tiles): bit-identical images."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for tag, env in (("fast", {}), ("sort", {"GSV_R1_BIN": "0", "GSV_R2_RANGES": "0"})):
+        f = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, "-c", _PATHS_SCRIPT, root, str(f)], check=True,
+                       env={**os.environ, **env}, timeout=600)
+        res[tag] = np.load(f)
+    assert np.array_equal(res["fast"], res["sort"])
