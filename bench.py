@@ -88,8 +88,11 @@ def make_inputs(a, seed):
     spec = benchmark_spec(a.gaussians, a.frames, a.group)
     cfg = EncodeConfig(layer_count=a.layers, prune_fraction=0.0, motion_threshold=0.0025)
     t0 = time.time()
+    import torch
+    # the GPU encoder when a device is present (byte-identical to the host coder)
     blobs = encode_stream(lambda: iter_frames(spec, seed), cfg, codecs=(0, 1),
-                          positions_source=lambda: iter_frames(spec, seed, positions_only=True))
+                          positions_source=lambda: iter_frames(spec, seed, positions_only=True),
+                          device=True if torch.cuda.is_available() else None)
     print(f"[bench] encoded {a.frames} frames x {a.gaussians} in {time.time() - t0:.1f}s",
           file=sys.stderr, flush=True)
     CACHE.mkdir(parents=True, exist_ok=True)

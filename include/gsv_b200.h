@@ -131,6 +131,14 @@ int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len,
  * bytes are staged and decoded; frames are numbered 0.. within the range. */
 int gsv_video_open_groups(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer, int g0,
                           int g1, gsv_video** out);
+/* an arbitrary list of groups (a shard of a sequence: e.g. the
+ * longest-processing-time assignment of groups to ranks), opened in list
+ * order; frames are numbered 0.. group after group in that order.  dev_data:
+ * NULL (stage the groups' layer-prefix bytes from `data`) or the whole
+ * container resident in HBM as for gsv_video_open_resident.  Groups must be
+ * in range and distinct. */
+int gsv_video_open_group_list(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
+                              int up_to_layer, const int32_t* groups, int ngroups, gsv_video** out);
 void gsv_video_close(gsv_video* v);
 int gsv_video_frame_count(const gsv_video* v);
 int gsv_video_decoded_layers(const gsv_video* v);
@@ -198,6 +206,12 @@ int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* po
                       const double* rot, const double* scl, const double* opac,
                       const double* sh, const gsv_camera* cam, int32_t* rects, double* depth,
                       int32_t* order, int32_t* tile_count, int64_t* n_visible);
+
+/* the same for frame t of a decoded video, through the production projection
+ * (integer codes dequantised in registers from the code planes) -- the path
+ * gsv_video_render and gsv_video_render_batch run */
+int gsv_video_project_debug(gsv_video* v, int t, const gsv_camera* cam, int32_t* rects, double* depth,
+                            int32_t* order, int32_t* tile_count, int64_t* n_visible);
 
 /* ---- codec (decode_planes, codec.py:226-263): one payload, host buffers --
  * hdr receives codec, bits, width, height, count; samples (count*h*w) as u32. */

@@ -92,6 +92,9 @@ _SIGS = {
     "gsv_video_open_groups": (_I, [_P, _P, _SZ, _I, _I, _I, ctypes.POINTER(_P)]),
     "gsv_video_open_resident": (_I, [_P, _P, _SZ, _P, _I, ctypes.POINTER(_P)]),
     "gsv_video_close": (None, [_P]),
+    "gsv_video_open_group_list": (_I, [_P, _P, _SZ, _P, _I, _P, _I, _P]),
+    "gsv_video_project_debug": (_I, [_P, _I, ctypes.POINTER(Camera_t), _P, _P, _P, _P,
+                                     ctypes.POINTER(_I64)]),
     "gsv_video_frame_count": (_I, [_P]),
     "gsv_video_decoded_layers": (_I, [_P]),
     "gsv_video_group_of": (_I, [_P, _I]),

@@ -166,22 +166,29 @@ def _read_prefix(f, up_to_layer: int | None):
     k = info.layer_count if up_to_layer is None else up_to_layer
     if not 1 <= k <= info.layer_count:
         raise InvalidInputError(f"layer {up_to_layer} out of range 1..{info.layer_count}")
-    end = 0
+    # payloads are read at their absolute offsets (read_layers seeks to
+    # entry.offset, container.py:282) while the header and directory come
+    # from the current position, as read_structure reads them
+    L = info.layer_count
+    hdr = 42 + sum(8 + 4 * L + sum(2 + 28 * len(g.channels[l]) for l in range(L)) for g in info.groups)
+    buf = bytearray(blob[:hdr])  # header + directory only (no payload bytes of any layer yet)
     for g in info.groups:
         for l in range(k):
             for e in g.channels[l]:
-                end = max(end, e.offset + e.size)
-    buf = bytearray(max(end, len(blob)))
-    buf[:len(blob)] = blob
-    for g in info.groups:
-        for l in range(k):
-            for e in g.channels[l]:
-                f.seek(start + e.offset)
+                f.seek(e.offset)
                 chunk = f.read(e.size)
-                buf[e.offset:e.offset + len(chunk)] = chunk
                 if len(chunk) < e.size:
-                    del buf[e.offset + len(chunk):]
+                    # a short read: end the buffer inside this entry so the
+                    # parser raises the reference's "unexpected end" for it
+                    if len(buf) > e.offset + len(chunk):
+                        del buf[e.offset + len(chunk):]
+                    else:
+                        buf.extend(bytes(e.offset - len(buf)))
+                        buf.extend(chunk)
                     return bytes(buf), info, k
+                if len(buf) < e.offset + e.size:
+                    buf.extend(bytes(e.offset + e.size - len(buf)))
+                buf[e.offset:e.offset + e.size] = chunk
     return bytes(buf), info, k
 
 
@@ -223,10 +230,12 @@ class DeviceVideo:
 
     def __init__(self, source, up_to_layer: int | None = None, session: Session | None = None,
                  resident: torch.Tensor | None = None, groups: tuple | None = None,
-                 info: ContainerInfo | None = None):
+                 info: ContainerInfo | None = None, group_list=None):
         """groups=(g0, g1): open only those groups (a streaming player's
         unit; only their bytes are staged and decoded, frames numbered from 0
-        within the range)."""
+        within the range).  group_list=[g, ...]: any set of groups (a rank's
+        shard of the sequence), in list order, frames numbered from 0 group
+        after group; works with a resident container too."""
         self.session = session or default_session()
         L = self.session.lib
         ptr = None
@@ -268,7 +277,18 @@ class DeviceVideo:
         nbytes = data.numel() if ptr is not None else len(data)
         hptr = ptr if ptr is not None else data
         self.group_range = None
-        if groups is not None:
+        self.group_list = None
+        if group_list is not None:
+            gl = [int(g) for g in group_list]
+            arr = (ctypes.c_int32 * max(1, len(gl)))(*gl)
+            check(L.gsv_video_open_group_list(self.session.handle, hptr, nbytes,
+                                              resident.data_ptr() if resident is not None else None,
+                                              k, arr, len(gl), ctypes.byref(h)))
+            self.group_list = tuple(gl)
+            info = ContainerInfo(info.version, info.layer_count, info.sh_degree, info.fps, info.bounds,
+                                 info.flags, tuple(info.groups[g] for g in gl))
+            self.info = info
+        elif groups is not None:
             g0, g1 = int(groups[0]), int(groups[1])
             if resident is not None:
                 raise InvalidInputError("groups= needs a host source")
@@ -400,6 +420,27 @@ class DeviceVideo:
                                              int(streams), check_)
         _lib.check(rc)
         _post(self.session)
+
+    def project_debug(self, t: int, cam):
+        """Projection outputs of frame t through the production projection
+        (codes dequantised in registers from the code planes, the path
+        render/render_batch run): rects (n,4; zeros when culled), fp64 depth
+        (n), order (depth rank -> splat index, survivors first, stable), tile
+        counts (n) and the survivor count."""
+        n = self.splat_count(t)
+        dev = torch.device("cuda", self.session.device)
+        rects = torch.zeros((n, 4), dtype=torch.int32, device=dev)
+        depth = torch.zeros((n,), dtype=torch.float64, device=dev)
+        order = torch.zeros((n,), dtype=torch.int32, device=dev)
+        tiles = torch.zeros((n,), dtype=torch.int32, device=dev)
+        nvis = ctypes.c_int64(0)
+        _pre(self.session)
+        check(self.lib.gsv_video_project_debug(self.handle, int(t), ctypes.byref(camera_struct(cam)),
+                                               _ptr(rects), _ptr(depth), _ptr(order), _ptr(tiles),
+                                               ctypes.byref(nvis)))
+        _post(self.session)
+        return (rects.cpu().numpy(), depth.cpu().numpy(), order.cpu().numpy(), tiles.cpu().numpy(),
+                int(nvis.value))
 
     def to_decoded_video(self) -> DecodedVideo:
         groups = []

@@ -50,10 +50,11 @@ def _stale(obj: Path, src: Path) -> bool:
 
 
 def build(verbose: bool = False, force: bool = False) -> Path:
+    from concurrent.futures import ThreadPoolExecutor
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
     objs = []
     relink = force or not LIB.exists()
-    logs = []
+    jobs = []
     for name, extra in SOURCES.items():
         src = CSRC / name
         obj = OBJ_DIR / (name + ".o")
@@ -62,12 +63,17 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             cmd = [nvcc(), "-c", str(src), "-o", str(obj), *NVCC_COMMON, *extra]
             if name.endswith(".cpp"):
                 cmd = [nvcc(), "-x", "cu", "-c", str(src), "-o", str(obj), *NVCC_COMMON]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            logs.append((name, r.stdout + r.stderr))
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {name}")
-            relink = True
+            jobs.append((name, cmd))
+    # translation units compile in parallel (independent objects)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(lambda j: (j[0], subprocess.run(j[1], capture_output=True, text=True)), jobs))
+    logs = []
+    for name, r in results:
+        logs.append((name, r.stdout + r.stderr))
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {name}")
+        relink = True
     if relink:
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [nvcc(), "-shared", *ARCH, "-o", str(tmp), *map(str, objs), "-cudart", "static"]

@@ -384,7 +384,7 @@ struct gsv_video {
 namespace {
 
 int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
-               int up_to_layer, gsv_video** out, int g0 = 0, int g1 = -1) {
+               int up_to_layer, gsv_video** out, const std::vector<int>* sel = nullptr) {
     *out = nullptr;
     t_stage.reset();
     static const bool dbg_t = getenv("GSV_DEBUG_OPEN_TIMING") != nullptr;  // dev: phase times to stderr
@@ -404,15 +404,25 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     };
     int rc = parse_container(data, len, &v->c);
     if (rc) return bail(rc);
-    if (g1 == -1) g1 = (int)v->c.groups.size();
-    if (g0 < 0 || g1 > (int)v->c.groups.size() || g0 >= g1)
-        return bail(fail(GSV_E_INVALID_INPUT, "group range [" + std::to_string(g0) + ", " + std::to_string(g1) +
-                                                  ") out of range 0.." + std::to_string(v->c.groups.size())));
-    if (g0 > 0 || g1 < (int)v->c.groups.size()) {  // keep the selected groups only (their bytes only are staged)
-        v->c.groups.erase(v->c.groups.begin() + g1, v->c.groups.end());
-        v->c.groups.erase(v->c.groups.begin(), v->c.groups.begin() + g0);
-        const uint32_t base = v->c.groups[0].start_frame;  // frames numbered from 0 in the range
-        for (GroupDir& gd : v->c.groups) gd.start_frame -= base;
+    if (sel) {  // keep the selected groups only, in list order (only their bytes are staged)
+        const int G0 = (int)v->c.groups.size();
+        if (sel->empty()) return bail(fail(GSV_E_INVALID_INPUT, "empty group list"));
+        std::vector<char> seen(G0, 0);
+        std::vector<GroupDir> keep;
+        for (int g : *sel) {
+            if (g < 0 || g >= G0)
+                return bail(fail(GSV_E_INVALID_INPUT,
+                                 "group " + std::to_string(g) + " out of range 0.." + std::to_string(G0 - 1)));
+            if (seen[g]) return bail(fail(GSV_E_INVALID_INPUT, "group " + std::to_string(g) + " listed twice"));
+            seen[g] = 1;
+            keep.push_back(v->c.groups[g]);
+        }
+        uint32_t next = 0;  // frames numbered from 0, group after group in list order
+        for (GroupDir& gd : keep) {
+            gd.start_frame = next;
+            next += gd.frame_count;
+        }
+        v->c.groups = std::move(keep);
     }
     const Container& c = v->c;
     const int L = c.layer_count;
@@ -434,7 +444,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
         for (int l = 0; l < k; l++)
             for (const Entry& e : c.groups[g].channels[l]) {
                 if (e.offset >= len) continue;
-                const uint64_t end = std::min<uint64_t>(e.offset + e.size, len);
+                const uint64_t end = e.size > len - e.offset ? len : e.offset + e.size;
                 if (!any) {
                     lo[g] = e.offset;
                     hi[g] = end;
@@ -481,7 +491,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                 const int64_t o = seq++;
                 char nm[96];
                 snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", g, l + 1, attr_name(e.attr), e.comp);
-                if (e.offset + e.size > len || e.offset > len) {
+                if (e.offset > len || e.size > len - e.offset) {
                     stop = {o, 0, GSV_E_FORMAT,
                             "unexpected end of container (wanted " + std::to_string(e.size) + " bytes)"};
                     break;
@@ -685,7 +695,24 @@ int gsv_video_open_resident(gsv_session* s, const uint8_t* data, size_t len, con
 int gsv_video_open_groups(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer, int g0, int g1,
                           gsv_video** out) {
     GSV_CUDA(cudaSetDevice(s->device));
-    return open_video(s, data, len, nullptr, up_to_layer, out, g0, g1);
+    *out = nullptr;
+    gsv_info info;
+    if (int rc = gsv_read_info(data, len, &info)) return rc;
+    if (g0 < 0 || g1 > info.group_count || g0 >= g1)
+        return fail(GSV_E_INVALID_INPUT, "group range [" + std::to_string(g0) + ", " + std::to_string(g1) +
+                                             ") out of range 0.." + std::to_string(info.group_count));
+    std::vector<int> sel;
+    for (int g = g0; g < g1; g++) sel.push_back(g);
+    return open_video(s, data, len, nullptr, up_to_layer, out, &sel);
+}
+
+int gsv_video_open_group_list(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
+                              int up_to_layer, const int32_t* groups, int ngroups, gsv_video** out) {
+    GSV_CUDA(cudaSetDevice(s->device));
+    *out = nullptr;
+    if (ngroups < 0 || (ngroups > 0 && !groups)) return fail(GSV_E_INVALID_INPUT, "invalid group list");
+    std::vector<int> sel(groups, groups + ngroups);
+    return open_video(s, data, len, dev_data, up_to_layer, out, &sel);
 }
 
 void gsv_video_close(gsv_video* v) {
@@ -903,30 +930,40 @@ int gsv_project_debug(gsv_session* s, int64_t n, int sh_degree, const double* po
                          s->stream);
 }
 
+int gsv_video_project_debug(gsv_video* v, int t, const gsv_camera* cam, int32_t* rects, double* depth,
+                            int32_t* order, int32_t* tile_count, int64_t* n_visible) {
+    FrameSrc src;
+    int rc = frame_src(v, t, &src);
+    if (rc) return rc;
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    return project_debug_planes(src, make_cam(*cam), &v->s->work, rects, depth, order, tile_count, n_visible,
+                                v->s->stream);
+}
+
 int gsv_fold_deltas(gsv_session* s, int64_t n, int shdim, double* pos, double* rot, double* scl,
                     double* opac, double* sh, int nd, const double* const* d_trans,
                     const double* const* d_rot, const double* const* d_scl,
                     const double* const* d_opac, const double* const* d_sh) {
     if (nd <= 0 || n <= 0) return GSV_OK;
-    int* bad = nullptr;
-    GSV_CUDA(cudaMalloc(&bad, sizeof(int)));
-    cudaMemsetAsync(bad, 0, sizeof(int), s->stream);
-    std::vector<FoldTab> tab(nd);
+    GSV_CUDA(cudaSetDevice(s->device));
+    t_stage.reset();
+    // the delta table and the zero-quaternion flag share one pooled block;
+    // the flag comes back through the pinned staging buffer
+    std::vector<FoldTab> tab(nd + 1);
     for (int d = 0; d < nd; d++) tab[d] = FoldTab{d_trans[d], d_rot[d], d_scl[d], d_opac[d], d_sh[d]};
+    tab[nd] = FoldTab{};  // zeroed: the flag word
     DevBuf d_tab;
     int rc = upload(d_tab, tab, s->stream);
-    if (rc) {
-        cudaFree(bad);
-        return rc;
-    }
+    if (rc) return rc;
+    int* bad = reinterpret_cast<int*>(d_tab.as<FoldTab>() + nd);
     launch_fold_all(n, shdim, pos, rot, scl, opac, sh, d_tab.as<FoldTab>(), nd, bad, s->stream);  // one pass
     count_launch(1);
-    int h = 0;
-    cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
-    cudaError_t e = cudaStreamSynchronize(s->stream);
-    cudaFree(bad);
-    if (e != cudaSuccess) return fail(GSV_E_CUDA, cudaGetErrorString(e));
-    if (h) return fail(GSV_E_INVALID_INPUT, "zero quaternion cannot be normalized");
+    int* h = reinterpret_cast<int*>(t_stage.reserve(sizeof(int), s->stream));
+    int hv = 0;
+    GSV_CUDA(cudaMemcpyAsync(h ? h : &hv, bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    if (h) hv = *h;
+    if (hv) return fail(GSV_E_INVALID_INPUT, "zero quaternion cannot be normalized");
     return GSV_OK;
 }
 

@@ -366,7 +366,9 @@ __global__ void __launch_bounds__(128, 5) composite_strip_kernel(
             for (int k = 0; k < 3; k++) {
                 const float x = fminf(fmaxf(v[k], 0.0f), 1.0f);
                 if (out_rgb) out_rgb[3 * pix + k] = x;
-                if (out_rgb8) out_rgb8[3 * pix + k] = (uint8_t)floorf(x * 255.0f + 0.5f);
+                // write_ppm's u8 = floor(p * 255 + 0.5) (render.py:165-169) of this
+                // fp32 value, exactly: x * 255 and + 0.5 are exact in fp64
+                if (out_rgb8) out_rgb8[3 * pix + k] = (uint8_t)floor(__dadd_rn(__dmul_rn((double)x, 255.0), 0.5));
             }
         }
         if (lane == 0 && !last) *flag = tsat ? kTileSaturated : kTileBlank;

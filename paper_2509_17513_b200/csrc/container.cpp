@@ -148,6 +148,7 @@ int parse_container(const uint8_t* data, size_t len, Container* out) {
     if (ci.layer_count < 1) return fail(GSV_E_FORMAT, "layer count must be >= 1");
     const int L = ci.layer_count;
     uint64_t last = 0;
+    bool last_inf = false;
     ci.groups.resize(ngroups);
     for (int g = 0; g < ngroups; g++) {
         GroupDir& gd = ci.groups[g];
@@ -180,8 +181,11 @@ int parse_container(const uint8_t* data, size_t len, Container* out) {
                 if (en.attr > 4) {
                     return fail(GSV_E_FORMAT, "unknown attribute code " + std::to_string(en.attr));
                 }
-                if (en.offset < last) return fail(GSV_E_FORMAT, "payload offsets are not increasing");
-                last = en.offset + en.size;
+                // offset + size as an unbounded integer (the reference's Python
+                // ints): a sum past 2^64 makes every later offset smaller
+                if (last_inf || en.offset < last) return fail(GSV_E_FORMAT, "payload offsets are not increasing");
+                last_inf = en.size > UINT64_MAX - en.offset;
+                last = last_inf ? UINT64_MAX : en.offset + en.size;
             }
         }
     }

@@ -71,6 +71,8 @@ int slot_of(int attr, int comp, int shdim);
 inline int slot_count(int sh_degree) { return 11 + 3 * (sh_degree + 1) * (sh_degree + 1); }
 constexpr int kMaxSlots = 11 + 48;
 constexpr int kMaxLayers = 64;
+constexpr int kMaxDevices = 64;  // per-device attribute state
+constexpr int kCtrWords = 32;  // device counters per render workspace
 
 // ---- device descriptors ------------------------------------------------------
 // One decodable (group, layer, entry) payload.
@@ -170,6 +172,8 @@ struct RenderWork {
     uint64_t* dkey[2] = {nullptr, nullptr};  // depth sort keys (ping-pong)
     uint32_t* didx[2] = {nullptr, nullptr};  // splat indices (ping-pong)
     SplatRec* rec = nullptr;                 // by splat index
+    uint64_t* tie_k = nullptr;               // depth tie fix-up of long runs: key scratch
+    uint32_t* tie_runs = nullptr;            // long runs of equal truncated keys (start, end)
     // per key
     uint32_t* tkey[2] = {nullptr, nullptr};
     uint32_t* tval[2] = {nullptr, nullptr};
@@ -280,6 +284,9 @@ int ssim_device(const void* a, const void* b, int H, int W, bool f64, double* ou
 int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
                   double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
                   cudaStream_t s);
+int project_debug_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
+                         double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
+                         cudaStream_t s);
 struct FoldTab {  // one frame delta (motion.py:58-141), device pointers
     const double* dt;
     const double* dq;

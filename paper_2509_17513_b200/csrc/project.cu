@@ -416,10 +416,11 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
 #undef GSV_PROJ
 }
 
-void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s) {
+void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s,
+                           int32_t* dbg_rect, double* dbg_depth) {
     init_quotient_tables();
     launch_project(PlaneLoader{src}, (int64_t)src.layer_off[src.nlayers], cam, src.sh_degree, w,
-                   nullptr, nullptr, s);
+                   dbg_rect, dbg_depth, s);
 }
 
 void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* dbg_rect,

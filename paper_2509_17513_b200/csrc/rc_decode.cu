@@ -51,7 +51,8 @@ void launch_copy_planes(const CopyJob* jobs, int njobs, cudaStream_t s) {
 // at a time from a 4-word register queue of aligned loads issued ~16 bytes
 // ahead.  Bytes past the block read as zero (_rc.py:129,150).
 struct CodedStream {
-    const uint32_t* wp;  // next aligned word to load
+    const uint32_t* wp;    // next aligned word to load
+    const uint32_t* wend;  // one past the last word holding a byte of the block
     uint32_t r0, r1, r2, r3;
     uint64_t bb;
     int32_t nbits;       // valid bits in bb
@@ -62,9 +63,13 @@ struct CodedStream {
         r0 = r1;
         r1 = r2;
         r2 = r3;
-        r3 = __ldg(wp++);
+        r3 = ld(wp++);
         return w;
     }
+    // words past the block are never loaded (they read as zero, like the
+    // reference's zero fill): a corrupt plane that decodes far beyond its
+    // coded bytes cannot walk off the staged buffer
+    __device__ __forceinline__ uint32_t ld(const uint32_t* p) const { return p < wend ? __ldg(p) : 0u; }
     // big-endian word with only its first m bytes kept
     __device__ __forceinline__ static uint32_t be_keep(uint32_t w_le, int32_t m) {
         const uint32_t be = __byte_perm(w_le, 0u, 0x0123);
@@ -73,11 +78,13 @@ struct CodedStream {
     __device__ __forceinline__ void init(const uint8_t* block, uint32_t len) {
         const uintptr_t s = reinterpret_cast<uintptr_t>(block) + 1;  // byte 0 is always zero
         wp = reinterpret_cast<const uint32_t*>(s & ~uintptr_t(3));
+        const uintptr_t e = reinterpret_cast<uintptr_t>(block) + (len ? len : 1);  // block end (exclusive)
+        wend = reinterpret_cast<const uint32_t*>((e + 3) & ~uintptr_t(3));
         const int k = (int)(s & 3);
-        r0 = __ldg(wp);
-        r1 = __ldg(wp + 1);
-        r2 = __ldg(wp + 2);
-        r3 = __ldg(wp + 3);
+        r0 = ld(wp);
+        r1 = ld(wp + 1);
+        r2 = ld(wp + 2);
+        r3 = ld(wp + 3);
         wp += 4;
         left = (int32_t)len - 1;
         const int nb = 4 - k;

@@ -16,20 +16,22 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "gsv_internal.h"
 #include "sort.cuh"
 
 namespace gsv {
 
-void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
+void launch_project_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s,
+                           int32_t* dbg_rect = nullptr, double* dbg_depth = nullptr);
 void launch_splat2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, cudaStream_t s);
 void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* dbg_rect,
                         double* dbg_depth, cudaStream_t s);
 
 enum { C_NVIS = 0, C_NKEYS = 1, C_DMIN = 2, C_DMAX = 3, C_OVF = 4, C_N = 5, C_KCLAMP = 6,
        C_RN = 7, C_NPASS = 8 /* int pair: passes, key shift */, C_MAXK = 9 /* sticky */,
-       C_TOTK = 10, C_EMITK = 11 };
+       C_TOTK = 10, C_EMITK = 11, C_LONGRUNS = 12 };
 
 CamDev make_cam(const gsv_camera& c) {
     CamDev d;
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ct
     ctr[C_RN] = 0;
     ctr[C_TOTK] = 0;
     ctr[C_EMITK] = 0;
+    ctr[C_LONGRUNS] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[0] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[1] = 0;
 }
@@ -128,12 +131,18 @@ __global__ void __launch_bounds__(256) depth_key_prep(uint64_t* __restrict__ ful
         if (h[p][threadIdx.x]) atomicAdd(&ghist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
 }
 
-// Stable order among equal key32 values by the full key: one thread per run
-// of equal key32 (insertion sort, stable).  Runs of distinct full keys need
-// depth differences below 2^-32 of the depth range, so they are short.
+// Stable order among equal key32 values by the full key.  The radix sort is
+// stable over splats in index order, so a run of equal key32 is in index
+// order and its exact order is (full key, index).  A thread per run start
+// finds the run's end by galloping (key32 is sorted); runs of up to 32 are
+// put in order by that thread (insertion sort), longer runs -- many distinct
+// depths sharing one truncated key, e.g. a far outlier stretching the depth
+// range -- are listed for depth_tie_long (a CTA per run).
+constexpr uint32_t kShortTieRun = 32;
 __global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t* __restrict__ k1,
                                 uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
-                                const uint64_t* __restrict__ full, const unsigned long long* __restrict__ ctr) {
+                                const uint64_t* __restrict__ full, unsigned long long* __restrict__ ctr,
+                                uint32_t* __restrict__ long_runs) {
     const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
     const int shift = reinterpret_cast<const int*>(ctr + C_NPASS)[1];
     if (shift == 0 || np == 0) return;
@@ -143,9 +152,26 @@ __global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t*
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         const uint32_t k = key[r];
         if (r > 0 && key[r - 1] == k) continue;
-        uint32_t e = r + 1;
-        while (e < n && key[e] == k) e++;
-        if (e - r < 2) continue;
+        if (r + 1 >= n || key[r + 1] != k) continue;
+        // upper bound of k in [r + 1, n): gallop, then bisect
+        uint32_t lo = r + 1, step = 1, hi = r + 2;
+        while (hi < n && key[hi] == k) {
+            lo = hi;
+            step *= 2;
+            hi = (n - lo > step) ? lo + step : n;
+        }
+        while (hi - lo > 1) {  // key[lo] == k, key[hi] != k (or hi == n)
+            const uint32_t m = lo + (hi - lo) / 2;
+            if (key[m] == k) lo = m;
+            else hi = m;
+        }
+        const uint32_t e = lo + 1;
+        if (e - r > kShortTieRun) {
+            const unsigned long long j = atomicAdd(ctr + C_LONGRUNS, 1ull);
+            long_runs[2 * j] = r;
+            long_runs[2 * j + 1] = e;
+            continue;
+        }
         const uint64_t f0 = full[idx[r]];
         bool same = true;
         for (uint32_t q = r + 1; q < e && same; q++) same = full[idx[q]] == f0;
@@ -160,6 +186,122 @@ __global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t*
             }
             idx[p] = v;
         }
+    }
+}
+
+// (full key, index) order
+__device__ __forceinline__ bool tie_less(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Long runs of equal key32: a CTA per run sorts (full key, index) pairs --
+// bitonic in shared memory per chunk of kTieChunk, then merge passes between
+// two global scratch buffers (merge path per thread) for longer runs.
+constexpr int kTieThreads = 256, kTieChunk = 2048;
+__global__ void __launch_bounds__(kTieThreads) depth_tie_long(uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
+                                                               const uint64_t* __restrict__ full,
+                                                               const unsigned long long* __restrict__ ctr,
+                                                               const uint32_t* __restrict__ long_runs,
+                                                               uint64_t* __restrict__ sk0, uint32_t* __restrict__ si0,
+                                                               uint64_t* __restrict__ sk1, uint32_t* __restrict__ si1) {
+    __shared__ uint64_t ks[kTieChunk];
+    __shared__ uint32_t is[kTieChunk];
+    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
+    const uint32_t nruns = (uint32_t)ctr[C_LONGRUNS];
+    uint32_t* idx = (np & 1) ? i1 : i0;
+    for (uint32_t j = blockIdx.x; j < nruns; j += gridDim.x) {
+        const uint32_t r = long_runs[2 * j], e = long_runs[2 * j + 1], L = e - r;
+        // 1) chunks of kTieChunk sorted in shared memory
+        for (uint32_t c0 = 0; c0 < L; c0 += kTieChunk) {
+            const uint32_t m = min((uint32_t)kTieChunk, L - c0);
+            uint32_t P = 1;
+            while (P < m) P *= 2;
+            for (uint32_t t = threadIdx.x; t < P; t += kTieThreads) {
+                if (t < m) {
+                    const uint32_t v = idx[r + c0 + t];
+                    is[t] = v;
+                    ks[t] = full[v];
+                } else {
+                    is[t] = 0xFFFFFFFFu;
+                    ks[t] = ~0ull;
+                }
+            }
+            __syncthreads();
+            for (uint32_t k = 2; k <= P; k *= 2)
+                for (uint32_t h = k / 2; h > 0; h /= 2) {
+                    for (uint32_t t = threadIdx.x; t < P / 2; t += kTieThreads) {
+                        const uint32_t a = 2 * h * (t / h) + (t % h), b = a + h;
+                        const bool up = (a & k) == 0;
+                        const bool gt = tie_less(ks[b], is[b], ks[a], is[a]);
+                        if (gt == up) {
+                            const uint64_t tk = ks[a];
+                            ks[a] = ks[b];
+                            ks[b] = tk;
+                            const uint32_t ti = is[a];
+                            is[a] = is[b];
+                            is[b] = ti;
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (uint32_t t = threadIdx.x; t < m; t += kTieThreads) {
+                if (L <= (uint32_t)kTieChunk) {
+                    idx[r + t] = is[t];
+                } else {
+                    sk0[r + c0 + t] = ks[t];
+                    si0[r + c0 + t] = is[t];
+                }
+            }
+            __syncthreads();
+        }
+        if (L <= (uint32_t)kTieChunk) continue;
+        // 2) merge passes: runs of w -> 2w, ping-pong between the scratch pairs
+        uint64_t* ka = sk0 + r;
+        uint32_t* ia = si0 + r;
+        uint64_t* kb = sk1 + r;
+        uint32_t* ib = si1 + r;
+        for (uint32_t w = kTieChunk; w < L; w *= 2) {
+            for (uint32_t s0 = 0; s0 < L; s0 += 2 * w) {
+                const uint32_t na = min(w, L - s0), nb = (L - s0 > w) ? min(w, L - s0 - w) : 0;
+                const uint64_t* xk = ka + s0;
+                const uint32_t* xi = ia + s0;
+                const uint64_t* yk = xk + na;
+                const uint32_t* yi = xi + na;
+                const uint32_t tot = na + nb, per = (tot + kTieThreads - 1) / kTieThreads;
+                const uint32_t o0 = min(tot, threadIdx.x * per), o1 = min(tot, o0 + per);
+                if (o0 < o1) {
+                    // merge path: first x index of the diagonal o0
+                    uint32_t lo = o0 > nb ? o0 - nb : 0, hi = min(o0, na);
+                    while (lo < hi) {
+                        const uint32_t mi = (lo + hi) / 2;  // take x[mi] before y[o0 - 1 - mi]?
+                        if (tie_less(yk[o0 - 1 - mi], yi[o0 - 1 - mi], xk[mi], xi[mi])) hi = mi;
+                        else lo = mi + 1;
+                    }
+                    uint32_t x = lo, y = o0 - lo;
+                    for (uint32_t o = o0; o < o1; o++) {
+                        const bool tx = y >= nb || (x < na && tie_less(xk[x], xi[x], yk[y], yi[y]));
+                        if (tx) {
+                            kb[s0 + o] = xk[x];
+                            ib[s0 + o] = xi[x];
+                            x++;
+                        } else {
+                            kb[s0 + o] = yk[y];
+                            ib[s0 + o] = yi[y];
+                            y++;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            uint64_t* tk = ka;
+            ka = kb;
+            kb = tk;
+            uint32_t* ti = ia;
+            ia = ib;
+            ib = ti;
+        }
+        for (uint32_t t = threadIdx.x; t < L; t += kTieThreads) idx[r + t] = ia[t];
+        __syncthreads();
     }
 }
 
@@ -593,6 +735,8 @@ void work_free(RenderWork* w) {
         free_ptr(w->tval[b]);
     }
     free_ptr(w->rec);
+    free_ptr(w->tie_k);
+    free_ptr(w->tie_runs);
     free_ptr(w->state);
     free_ptr(w->tile_done);
     free_ptr(w->open_mask);
@@ -608,10 +752,10 @@ void work_free(RenderWork* w) {
 
 int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
     if (!w->ctr) {
-        GSV_CUDA(cudaMalloc(&w->ctr, 16 * sizeof(unsigned long long)));
-        GSV_CUDA(cudaMallocHost(&w->h_ctr, 16 * sizeof(unsigned long long)));
-        GSV_CUDA(cudaMemset(w->ctr, 0, 16 * sizeof(unsigned long long)));
-        memset(w->h_ctr, 0, 16 * sizeof(unsigned long long));
+        GSV_CUDA(cudaMalloc(&w->ctr, kCtrWords * sizeof(unsigned long long)));
+        GSV_CUDA(cudaMallocHost(&w->h_ctr, kCtrWords * sizeof(unsigned long long)));
+        GSV_CUDA(cudaMemset(w->ctr, 0, kCtrWords * sizeof(unsigned long long)));
+        memset(w->h_ctr, 0, kCtrWords * sizeof(unsigned long long));
     }
     n = std::max<int64_t>(n, 1);
     if (n > w->cap_n) {
@@ -624,6 +768,10 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         }
         free_ptr(w->rec);
         GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
+        free_ptr(w->tie_k);
+        free_ptr(w->tie_runs);
+        GSV_CUDA(cudaMalloc(&w->tie_k, c * sizeof(uint64_t)));
+        GSV_CUDA(cudaMalloc(&w->tie_runs, (c / (kShortTieRun + 1) + 1) * 2 * sizeof(uint32_t)));
         free_ptr(w->status);
         const size_t ns = (size_t)(c / 256 + 4) * sizeof(unsigned long long) + 64;
         GSV_CUDA(cudaMalloc(&w->status, ns));
@@ -724,6 +872,24 @@ static bool later_ranges() {  // dev toggle GSV_R2_RANGES
     return v != 0;
 }
 
+// Dynamic shared memory above 48 KB for the round-1 binning kernels.  The
+// attribute is per device, so the largest size unlocked so far is tracked per
+// device (atomically: several host threads may render on one device).
+static int r1_smem_attr(size_t sm) {
+    if (sm <= 48 * 1024) return GSV_OK;
+    static std::atomic<size_t> unlocked[kMaxDevices];
+    int dev = 0;
+    GSV_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) return fail(GSV_E_CUDA, "device ordinal out of range");
+    size_t cur = unlocked[dev].load();
+    if (sm <= cur) return GSV_OK;
+    GSV_CUDA(cudaFuncSetAttribute(r1_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    GSV_CUDA(cudaFuncSetAttribute(r1_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    while (cur < sm && !unlocked[dev].compare_exchange_weak(cur, sm)) {
+    }
+    return GSV_OK;
+}
+
 static int r1_reserve(RenderWork* w, size_t bc_words, size_t off_words) {
     if (bc_words > w->r1_bc_cap) {
         free_ptr(w->r1_bc);
@@ -817,6 +983,14 @@ static unsigned debug_skip() {
     return mask;
 }
 
+// exact order among ties of the truncated depth key (2 launches)
+static void launch_tie_fixup(RenderWork* w, cudaStream_t s) {
+    depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], w->ctr,
+                                             w->tie_runs);
+    depth_tie_long<<<148, kTieThreads, 0, s>>>(w->didx[0], w->didx[1], w->dkey[0], w->ctr, w->tie_runs, w->dkey[1],
+                                               w->tval[0], w->tie_k, w->tval[1]);
+}
+
 // Enqueue one frame.  `project` enqueues the projection kernel into w.
 template <class Proj>
 static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj project,
@@ -837,7 +1011,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     if (!(skip & 16)) project();
     if (dbl & 16) {  // the second projection counts into spare counter slots
         unsigned long long* keep = w->ctr;
-        w->ctr = keep + 12;
+        w->ctr = keep + 16;
         project();
         w->ctr = keep;
     }
@@ -849,10 +1023,9 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
         if (dbl & 4)
             radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
-        depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
-        if (dbl & 64)
-            depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
-        count_launch(2 + radix_launches(depth_key_bits() / 8, true));
+        launch_tie_fixup(w, s);
+        if (dbl & 64) launch_tie_fixup(w, s);
+        count_launch(3 + radix_launches(depth_key_bits() / 8, true));
     }
     prof_mark(ST_EMIT, s);
     std::vector<uint32_t> bounds;
@@ -887,12 +1060,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             int rc = r1_reserve(w, (size_t)nblk * ntiles, (size_t)ntiles + 1);
             if (rc) return rc;
             const size_t sm = (size_t)ntiles * 4;
-            static size_t sm_set = 48 * 1024;
-            if (sm > sm_set) {
-                cudaFuncSetAttribute(r1_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                cudaFuncSetAttribute(r1_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                sm_set = sm;
-            }
+            if (int rc = r1_smem_attr(sm)) return rc;
             r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, mask,
                                                   w->r1_bc);
             r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 32 * ((nblk + 31) / 32), 0, s>>>(w->r1_bc, (int)nblk, ntiles,
@@ -938,14 +1106,14 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
     prof_mark(ST_COUNT, s);
     // counters to the pinned mirror (a frame-parallel batch reads them back
     // once per stream at its end instead: the key-capacity maximum is sticky)
-    if (readback) cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    if (readback) cudaMemcpyAsync(w->h_ctr, ctr, kCtrWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     GSV_CUDA(cudaGetLastError());
     return GSV_OK;
 }
 
 int readback_counters(RenderWork* w, cudaStream_t s) {
     if (!w->ctr) return GSV_OK;
-    GSV_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, kCtrWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     return GSV_OK;
 }
 
@@ -1154,10 +1322,12 @@ __global__ void copy_order(const uint32_t* __restrict__ idx0, const uint32_t* __
     }
 }
 
-int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
-                  double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
-                  cudaStream_t s) {
-    const int64_t n = src.n;
+// Projection outputs of one splat source for parity tests: rects, fp64
+// depth, the stable depth order and per-splat tile counts, through the same
+// projection and depth-sort kernels as a render.
+template <class Proj>
+static int project_debug_impl(int64_t n, RenderWork* w, Proj project, int32_t* order, int32_t* tile_count,
+                              int64_t* n_visible, cudaStream_t s) {
     int rc = work_reserve(w, n, std::max<int64_t>(w->cap_k, n), 1, 0);
     if (rc) return rc;
     unsigned long long* ctr = w->ctr;
@@ -1165,18 +1335,36 @@ int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* 
     const SortScratch sc = sort_scratch(w);
     reset_frame_kernel<<<1, 256, 0, s>>>(ctr, (long long)n, sc.ghist, reinterpret_cast<uint32_t*>(w->tile_done), 0,
                                           0u);
-    launch_project_soa(src, cam, w, rects, depth, s);
+    project();
     if (n > 0) {
         depth_key_prep<<<prep_grid(n), 256, 0, s>>>(w->dkey[0], w->tkey[0], ctr, sc.ghist, depth_key_bits());
         radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
-        depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], ctr);
+        launch_tie_fixup(w, s);
         copy_order<<<148 * 4, 256, 0, s>>>(w->didx[0], w->didx[1], ctr, order, w->rec, tile_count);
     }
-    cudaMemcpyAsync(w->h_ctr, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(w->h_ctr, ctr, kCtrWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     GSV_CUDA(cudaStreamSynchronize(s));
     GSV_CUDA(cudaGetLastError());
     if (n_visible) *n_visible = (int64_t)w->h_ctr[C_NVIS];
     return GSV_OK;
+}
+
+int project_debug(const SoaSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
+                  double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
+                  cudaStream_t s) {
+    // the rects and depths are only needed until the work buffers are sized
+    int rc = work_reserve(w, src.n, std::max<int64_t>(w->cap_k, src.n), 1, 0);
+    if (rc) return rc;
+    return project_debug_impl(src.n, w, [&]() { launch_project_soa(src, cam, w, rects, depth, s); }, order,
+                              tile_count, n_visible, s);
+}
+
+int project_debug_planes(const FrameSrc& src, const CamDev& cam, RenderWork* w, int32_t* rects,
+                         double* depth, int32_t* order, int32_t* tile_count, int64_t* n_visible,
+                         cudaStream_t s) {
+    const int64_t n = src.layer_off[src.nlayers];
+    return project_debug_impl(n, w, [&]() { launch_project_planes(src, cam, w, s, rects, depth); }, order,
+                              tile_count, n_visible, s);
 }
 
 }  // namespace gsv

@@ -374,3 +374,25 @@ def test_binning_and_sort_paths_render_identically(tmp_path):
                        env={**os.environ, **env}, timeout=600)
         res[tag] = np.load(f)
     assert np.array_equal(res["fast"], res["sort"])
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+def test_truncated_coded_block_is_codec_error(gsvb, bits):
+    """A range-coded plane whose coded block is far shorter than the plane
+    needs (4 bytes for 4M samples): the decoder zero-fills past the block
+    like the reference (_rc.py:129,150) without reading past it, and the CRC
+    mismatch raises CodecError -- no illegal address, the context stays
+    usable."""
+    import struct
+    w = h = 2048
+    block = bytes([0x00, 0x9C, 0x41, 0x07])
+    body = bytes([0, 0]) + struct.pack("<I", len(block)) + block
+    blob = struct.pack("<BBHHHHI", 1, bits, w, h, 1, 0, len(body)) + body + struct.pack("<I", 0x12345678)
+    payload, end = gsvb.CodedPayload.from_bytes(blob)
+    assert end == len(blob)
+    with pytest.raises(gsvb.CodecError, match="checksum mismatch"):
+        gsvb.decode_planes(payload)
+    # the device is still healthy: a good payload decodes afterwards
+    d = json.loads((GOLDEN / "conformance" / "rc_u8_random.json").read_text())
+    good, _ = gsvb.CodedPayload.from_bytes(base64.b64decode(d["payload_b64"]))
+    assert gsvb.decode_planes(good)[0].samples.ravel().tolist() == d["expected_samples"][0]
