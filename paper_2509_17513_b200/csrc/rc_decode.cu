@@ -48,47 +48,67 @@ void launch_copy_planes(const CopyJob* jobs, int njobs, cudaStream_t s) {
 // Coded bytes as a big-endian bit buffer: the next byte sits in bits 63..56
 // of `bb`, so a renormalisation by `sh` (0, 8 or 16) bits is one funnel
 // shift into `code` plus a 64-bit shift of `bb`.  `bb` is refilled 32 bits
-// at a time from a 4-word register queue of aligned loads issued ~16 bytes
-// ahead.  Bytes past the block read as zero (_rc.py:129,150).
-struct CodedStream {
-    const uint32_t* wp;    // next aligned word to load
-    const uint32_t* wend;  // one past the last word holding a byte of the block
-    uint32_t r0, r1, r2, r3;
-    uint64_t bb;
-    int32_t nbits;       // valid bits in bb
-    int32_t left;        // stream bytes not yet moved into bb (<= 0: zero fill)
+// at a time from a lane-private ring of 4 x 16 B in shared memory that
+// cp.async keeps 3 chunks ahead of the read position.  (A queue of loaded
+// registers was slower: the compiler's loop-carried copies read each load
+// right after issuing it, so every refill waited out a global load; the
+// async copies never tie a register to an in-flight load.)  Bytes past the
+// block read as zero (_rc.py:129,150) and are never fetched.
+constexpr uint32_t kRingBytes = 64;  // per lane
 
-    __device__ __forceinline__ uint32_t pop() {
-        const uint32_t w = r0;
-        r0 = r1;
-        r1 = r2;
-        r2 = r3;
-        r3 = ld(wp++);
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+struct CodedStream {
+    const uint8_t* gp;    // next 16-B chunk (global, aligned) to fetch
+    const uint8_t* gend;  // one past the last chunk holding a byte of the block
+    uint32_t ring;        // this lane's ring (shared address)
+    uint32_t rpos;        // ring offset of the next word to take
+    uint64_t bb;
+    int32_t nbits;        // valid bits in bb
+    int32_t left;         // stream bytes not yet moved into bb (<= 0: zero fill)
+
+    // one 16-B chunk into ring slot `slot` (zero-filled past the block)
+    __device__ __forceinline__ void fetch(uint32_t slot) {
+        const bool in = gp < gend;
+        const uint8_t* src = in ? gp : gend - 16;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;" ::"r"(ring + slot),
+                     "l"(src), "r"(in ? 16 : 0)
+                     : "memory");
+        gp += 16;
+    }
+    __device__ __forceinline__ uint32_t take_word() {
+        const uint32_t w = lds_u32(ring + rpos);
+        rpos = (rpos + 4) & (kRingBytes - 1);
+        if ((rpos & 15) == 0) {  // a chunk is used up: refetch 4 chunks ahead into its slot
+            fetch((rpos - 16) & (kRingBytes - 1));
+            // the chunk being entered was fetched 3 commits ago
+            asm volatile("cp.async.wait_group 3;" ::: "memory");
+        }
         return w;
     }
-    // words past the block are never loaded (they read as zero, like the
-    // reference's zero fill): a corrupt plane that decodes far beyond its
-    // coded bytes cannot walk off the staged buffer
-    __device__ __forceinline__ uint32_t ld(const uint32_t* p) const { return p < wend ? __ldg(p) : 0u; }
     // big-endian word with only its first m bytes kept
     __device__ __forceinline__ static uint32_t be_keep(uint32_t w_le, int32_t m) {
         const uint32_t be = __byte_perm(w_le, 0u, 0x0123);
         return m >= 4 ? be : (m > 0 ? be & ~(0xFFFFFFFFu >> (8 * m)) : 0u);
     }
-    __device__ __forceinline__ void init(const uint8_t* block, uint32_t len) {
+    __device__ __forceinline__ void init(const uint8_t* block, uint32_t len, uint32_t ring_addr) {
+        finish();  // no copy of the previous plane may still land in the ring
         const uintptr_t s = reinterpret_cast<uintptr_t>(block) + 1;  // byte 0 is always zero
-        wp = reinterpret_cast<const uint32_t*>(s & ~uintptr_t(3));
         const uintptr_t e = reinterpret_cast<uintptr_t>(block) + (len ? len : 1);  // block end (exclusive)
-        wend = reinterpret_cast<const uint32_t*>((e + 3) & ~uintptr_t(3));
-        const int k = (int)(s & 3);
-        r0 = ld(wp);
-        r1 = ld(wp + 1);
-        r2 = ld(wp + 2);
-        r3 = ld(wp + 3);
-        wp += 4;
+        gp = reinterpret_cast<const uint8_t*>(s & ~uintptr_t(15));
+        gend = reinterpret_cast<const uint8_t*>((e + 15) & ~uintptr_t(15));
+        ring = ring_addr;
+        for (uint32_t c = 0; c < 4; c++) fetch(16 * c);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        const int k = (int)(s & 15);
+        rpos = (uint32_t)(k & ~3);
         left = (int32_t)len - 1;
-        const int nb = 4 - k;
-        const uint32_t be = __byte_perm(pop(), 0u, 0x0123) << (8 * k);  // first nb bytes on top
+        const int b = k & 3, nb = 4 - b;
+        const uint32_t be = __byte_perm(take_word(), 0u, 0x0123) << (8 * b);  // first nb bytes on top
         const int32_t m = left < nb ? left : nb;
         const uint32_t kept = m >= 4 ? be : (m > 0 ? be & ~(0xFFFFFFFFu >> (8 * m)) : 0u);
         left -= nb;
@@ -98,7 +118,7 @@ struct CodedStream {
     }
     __device__ __forceinline__ void refill() {
         if (nbits <= 32) {
-            const uint32_t w = be_keep(pop(), left);
+            const uint32_t w = be_keep(take_word(), left);
             left -= 4;
             bb |= (uint64_t)w << (32 - nbits);
             nbits += 32;
@@ -110,6 +130,8 @@ struct CodedStream {
         nbits -= 32;
         return v;
     }
+    // drain the async copies of a finished plane (the ring is reused)
+    __device__ __forceinline__ void finish() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 };
 
 // Probabilities: lane-private, tree after tree, node n of a tree at byte
@@ -341,11 +363,8 @@ __device__ __forceinline__ uint32_t decode_byte_v2(uint32_t T, uint32_t Tn, uint
     return ctx & 0xFFu;
 }
 
-__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
+// fixed point of the zero-branch adaptation p += (4096 - p) >> 4
+constexpr uint32_t kZeroSat = 4081u;
 
 // Variant 3: zero-prefix test.  Along the all-zero path of a bit tree
 // (nodes 1, 2, 4, ..., 2^(M-1)) a 0 decision leaves `code` alone and sets
@@ -359,8 +378,9 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 // the test fails the byte is decoded by variant 2 from the untouched state.
 template <int M, bool SAME_TREE>
 __device__ __forceinline__ uint32_t decode_byte_v3(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng,
-                                                   uint32_t& code, CodedStream& cs) {
+                                                   uint32_t& code, CodedStream& cs, bool* sat = nullptr) {
     static_assert(M >= 2 && M <= 8, "zero prefix length");
+    if (sat) *sat = false;  // set again below when the zero path ends saturated
     const uint32_t bhi = (uint32_t)(cs.bb >> 32);
     uint32_t z[M + 1];  // zero-path probabilities (z[M]: the node decision M starts at)
     z[0] = q0.y;
@@ -453,6 +473,12 @@ __device__ __forceinline__ uint32_t decode_byte_v3(uint32_t T, uint32_t Tn, uint
     const uint32_t used = 0x2107u - sel;
 #pragma unroll
     for (int k = 0; k < 8; k++) sts_u32(na[k], pn[k]);
+    if (sat) {
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < M; k++) all = all && pn[k] == kZeroSat;
+        *sat = all;
+    }
     const uint32_t ctx = M < 8 ? (node - T) >> 2 : 256u;
     if (SAME_TREE) {  // first decision was 0: nodes 1 and 2 were updated
         qn.y = pn[0];
@@ -469,7 +495,7 @@ __device__ __forceinline__ uint32_t decode_byte_v3(uint32_t T, uint32_t Tn, uint
 // advanced past a zero byte, or false and nothing touched (the caller then
 // decodes the byte with its single variant-2 instance).
 __device__ __forceinline__ bool zero_byte(uint32_t T, uint32_t Tn, uint4& q0, uint32_t& rng, uint32_t& code,
-                                          CodedStream& cs) {
+                                          CodedStream& cs, bool* sat = nullptr) {
     const uint32_t bhi = (uint32_t)(cs.bb >> 32);
     uint32_t z[8];
     z[0] = q0.y;
@@ -493,13 +519,142 @@ __device__ __forceinline__ bool zero_byte(uint32_t T, uint32_t Tn, uint4& q0, ui
     S += lt24 ? 1u : 0u;
     rng = lt24 ? bound << 8 : bound;
     code = __funnelshift_lc(bhi, code, 8u * S);
+    bool all = true;
 #pragma unroll
-    for (int k = 0; k < 8; k++) sts_u32(T + 4u * (1u << k), z[k] + ((4096u - z[k]) >> 4));
+    for (int k = 0; k < 8; k++) {
+        const uint32_t pk = z[k] + ((4096u - z[k]) >> 4);
+        all = all && pk == kZeroSat;
+        sts_u32(T + 4u * (1u << k), pk);
+    }
+    if (sat) *sat = all;
     q0 = qn;
     cs.bb <<= 8 * S;
     cs.nbits -= (int32_t)(8 * S);
     cs.refill();
     return true;
+}
+
+// One full binary decision (the variant-2 step) as a function: bound,
+// compare, interval update, renormalisation by a predicated byte permute,
+// adapted probability, the child's probability and node address.
+__device__ __forceinline__ void rc_step(uint32_t& a, uint32_t& rng, uint32_t& code, uint32_t& sel, uint32_t& rmin,
+                                        uint32_t& pn, uint32_t& p, uint32_t& node, uint32_t& pbit, uint32_t bhi,
+                                        uint32_t c0, uint32_t c1, uint32_t c0T, uint32_t c1T) {
+    uint32_t bitv, nnode;
+    asm("{\n\t"
+        ".reg .pred pb, pl;\n\t"
+        ".reg .u32 bnd, r1, r, t4, t12, K, d, off;\n\t"
+        "mul.lo.u32 bnd, %0, %9;\n\t"
+        "setp.ge.u32 pb, %2, bnd;\n\t"
+        "sub.u32 r1, %1, bnd;\n\t"
+        "selp.u32 r, r1, bnd, pb;\n\t"
+        "@pb sub.u32 %2, %2, bnd;\n\t"
+        "setp.lt.u32 pl, r, 16777216;\n\t"
+        "min.u32 %4, %4, r;\n\t"
+        "shr.u32 t4, r, 4;\n\t"
+        "shr.u32 t12, r, 12;\n\t"
+        "selp.u32 %0, t4, t12, pl;\n\t"
+        "@pl shl.b32 r, r, 8;\n\t"
+        "@pl prmt.b32 %2, %2, %10, %3;\n\t"
+        "@pl sub.u32 %3, %3, 1;\n\t"
+        "mov.u32 %1, r;\n\t"
+        "selp.u32 K, 15, 4096, pb;\n\t"
+        "sub.s32 d, K, %9;\n\t"
+        "shr.s32 d, d, 4;\n\t"
+        "add.u32 %5, %9, d;\n\t"
+        "selp.u32 %6, %12, %11, pb;\n\t"
+        "selp.u32 off, %14, %13, pb;\n\t"
+        "mad.lo.u32 %7, %15, 2, off;\n\t"
+        "selp.u32 %8, 1, 0, pb;\n\t"
+        "}"
+        : "+r"(a), "+r"(rng), "+r"(code), "+r"(sel), "+r"(rmin), "=r"(pn), "=r"(p), "=r"(nnode), "=r"(bitv)
+        : "r"(p), "r"(bhi), "r"(c0), "r"(c1), "r"(c0T), "r"(c1T), "r"(node));
+    node = nnode;
+    pbit = bitv;
+}
+
+// Variant 4: the zero-prefix tests of variant 3 once their path is
+// SATURATED.  A zero decision moves p to p + ((4096 - p) >> 4), whose fixed
+// point is 4081; after ~50 zero prefixes in a row (position high bytes are
+// always zero, 8-bit residuals always have a zero top nibble) every node on
+// the zero path holds 4081 and stays there.  A lane-private flag records
+// that state, and then M zero decisions are exactly: bounds b_k = (b_{k-1} >>
+// 12) * 4081 while no renormalisation intervenes (b_{M-2} >= 2^24: bounds
+// decrease), and the path is taken iff code < b_{M-1}.  That is M
+// multiply-shift pairs and two compares -- no probability loads, no
+// adaptation, no stores.  Anything else (not saturated, a bound below 2^24
+// before the last decision, the code above the bound) goes to the exact
+// variant-3 path, which also re-derives the flag.
+__device__ __forceinline__ bool zero_byte_sat(uint32_t Tn, uint4& q0, uint32_t& rng, uint32_t& code,
+                                              CodedStream& cs) {
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t b = shr_opaque<12>(rng) * kZeroSat, bp = b;
+#pragma unroll
+    for (int k = 1; k < 8; k++) {
+        bp = b;
+        b = shr_opaque<12>(b) * kZeroSat;
+    }
+    if (!(bp >= (1u << 24) && code < b)) return false;
+    q0 = lds_quad(Tn);
+    const uint32_t S = b < (1u << 24) ? 1u : 0u;  // b > 2^16: one renormalisation at most
+    rng = S ? b << 8 : b;
+    code = S ? __byte_perm(code, bhi, 0x2107u) : code;  // (code << 8) | next stream byte
+    cs.bb <<= 8 * S;
+    cs.nbits -= (int32_t)(8 * S);
+    cs.refill();
+    return true;
+}
+
+// 1-byte samples: a saturated 4-decision zero prefix (top nibble), then the
+// 4 low decisions as variant 2 does them; otherwise variant 3.
+__device__ __forceinline__ uint32_t decode_byte_v4(uint32_t T, uint4& q0, uint32_t& rng, uint32_t& code,
+                                                   CodedStream& cs, bool& sat) {
+    constexpr int M = 4;
+    if (sat) {
+        const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+        uint32_t p = lds_u32(T + 4u * (1u << M));           // node 16
+        uint4 cq = lds_quad(T + 16u * (1u << (M - 1)));     // its children 32, 33
+        uint4 nq = lds_quad(T + 16u * (1u << M));           // its grandchildren 64..67
+        uint32_t b = shr_opaque<12>(rng) * kZeroSat, bp = b;
+#pragma unroll
+        for (int k = 1; k < M; k++) {
+            bp = b;
+            b = shr_opaque<12>(b) * kZeroSat;
+        }
+        if (bp >= (1u << 24) && code < b) {
+            const uint32_t rng0 = rng, code0 = code;
+            const uint32_t S = b < (1u << 24) ? 1u : 0u;
+            rng = S ? b << 8 : b;
+            code = S ? __byte_perm(code, bhi, 0x2107u) : code;
+            uint32_t a = rng >> 12, sel = 0x2107u - S, rmin = 0xFFFFFFFFu;
+            uint32_t node = T + 4u * (1u << M), pbit = 0u, pn[8 - M], na[8 - M];
+            const uint32_t m3T = 0u - 3u * T, c0T = 0u - T, c1T = 4u - T;
+#pragma unroll
+            for (int k = M; k < 8; k++) {
+                uint4 nn = make_uint4(0u, 0u, 0u, 0u);
+                if (k == M) nn = nq;
+                else if (k < 6) nn = lds_quad(4u * node + m3T);
+                na[k - M] = node;
+                const uint32_t c0 = pbit ? cq.z : cq.x, c1 = pbit ? cq.w : cq.y;
+                rc_step(a, rng, code, sel, rmin, pn[k - M], p, node, pbit, bhi, c0, c1, c0T, c1T);
+                cq = nn;
+            }
+            const uint32_t used = 0x2107u - sel;
+            if (rmin < (1u << 16) || used > 4u) {  // rare: the careful path redoes the byte
+                rng = rng0;
+                code = code0;
+                sat = false;
+                return decode_byte_slow(T, T, q0, rng, code, cs);
+            }
+#pragma unroll
+            for (int k = 0; k < 8 - M; k++) sts_u32(na[k], pn[k]);
+            cs.bb <<= 8 * used;
+            cs.nbits -= (int32_t)(8 * used);
+            cs.refill();
+            return ((node - T) >> 2) & 0xFFu;  // q0 unchanged: nodes 1 and 2 still hold 4081
+        }
+    }
+    return decode_byte_v3<M, true>(T, T, q0, rng, code, cs, &sat);
 }
 
 template <int V, bool SAME_TREE>
@@ -510,14 +665,14 @@ __device__ __forceinline__ uint32_t decode_byte_v(uint32_t T, uint32_t Tn, uint4
 }
 
 template <int V, int NB, bool PREV>
-__device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
+__device__ __forceinline__ void decode_plane(uint32_t P, uint32_t R, const PlaneRef& pr,
                                              const uint32_t* __restrict__ prev,
-                                             uint32_t* __restrict__ out, uint32_t hw, uint32_t w) {
+                                             uint32_t* __restrict__ out, uint32_t hw, uint32_t w, bool& sat) {
     constexpr int SPW = 4 / NB;  // samples per 32-bit word
     constexpr uint32_t mask = NB == 4 ? 0xFFFFFFFFu : ((1u << (8 * NB)) - 1u);
     constexpr uint32_t def = 128u << (8 * NB - 8);
     CodedStream cs;
-    cs.init(pr.coded, pr.coded_len);
+    cs.init(pr.coded, pr.coded_len, R);
     uint32_t code = cs.take32();
     cs.refill();
     uint32_t rng = 0xFFFFFFFFu;
@@ -542,14 +697,23 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
             // so the loop body stays small in the instruction cache
             // (variant 3, 2-byte samples: one sample per iteration, the high
             // byte by the zero test with a cold variant-2 fallback)
-            constexpr int BPI = (V == 3 && NB == 2) ? 2 : 1;
+            constexpr int BPI = (V >= 3 && NB == 2) ? 2 : 1;
 #pragma unroll 1
             for (int e = 0; e < SPW * NB; e += BPI) {
                 const int j = e / NB, b = e % NB;
                 if (SPW > 1 && idx >= hw) break;
                 const uint32_t T = P + (uint32_t)b * kTreeBytes;
                 const uint32_t Tn = NB == 1 ? T : P + (uint32_t)((b + 1) % NB) * kTreeBytes;
-                if (V == 3 && NB == 2) {
+                if (V == 4 && NB == 2) {
+                    const uint32_t T1 = P + kTreeBytes;
+                    z = decode_byte_v2<false>(P, T1, q0, rng, code, cs);
+                    if (!(sat && zero_byte_sat(P, q0, rng, code, cs)) && !zero_byte(T1, P, q0, rng, code, cs, &sat)) {
+                        z |= decode_byte_v2<false>(T1, P, q0, rng, code, cs) << 8;
+                        sat = false;
+                    }
+                } else if (V == 4 && NB == 1) {
+                    z = decode_byte_v4(T, q0, rng, code, cs, sat);
+                } else if (V == 3 && NB == 2) {
                     const uint32_t T1 = P + kTreeBytes;
                     z = decode_byte_v2<false>(P, T1, q0, rng, code, cs);
                     if (!zero_byte(T1, P, q0, rng, code, cs)) z |= decode_byte_v2<false>(T1, P, q0, rng, code, cs) << 8;
@@ -588,7 +752,8 @@ __device__ __forceinline__ void decode_plane(uint32_t P, const PlaneRef& pr,
 // the warps land on separate SMs.
 template <int V, int NB>
 __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, const uint32_t* __restrict__ rc_runs,
-                                            int n, int blk, const PlaneRef* __restrict__ planes, uint32_t P) {
+                                            int n, int blk, const PlaneRef* __restrict__ planes, uint32_t P,
+                                            uint32_t R) {
     const int lane = threadIdx.x;
     for (int b = 0; b < NB; b++)  // new_bittree_probs (_rc.py:304-317)
         for (uint32_t i = 0; i < 256; i++)
@@ -597,15 +762,16 @@ __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, co
     if (gi >= n) return;
     const RunDesc r = runs[rc_runs[gi]];
     const uint32_t hw = (uint32_t)r.w * r.h;
+    bool sat = false;  // variant 4: zero-path probabilities saturated (persists with the model)
     for (int f = 0; f < r.count; f++) {
         const PlaneRef pr = planes[r.plane_base + f];
         if (pr.mode != 0) continue;  // RAW plane (already copied to aligned storage)
         uint32_t* out = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(pr.samples));
         if (f > 0) {
             const uint32_t* prev = reinterpret_cast<const uint32_t*>(planes[r.plane_base + f - 1].samples);
-            decode_plane<V, NB, true>(P, pr, prev, out, hw, r.w);
+            decode_plane<V, NB, true>(P, R, pr, prev, out, hw, r.w, sat);
         } else {
-            decode_plane<V, NB, false>(P, pr, nullptr, out, hw, r.w);
+            decode_plane<V, NB, false>(P, R, pr, nullptr, out, hw, r.w, sat);
         }
     }
 }
@@ -623,10 +789,13 @@ __global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restri
     extern __shared__ uint4 probs_s[];
     const int b = blockIdx.x;
     const int nb = b < c.blk[1] ? 1 : (b < c.blk[2] ? 2 : 4);
-    const uint32_t P = (uint32_t)__cvta_generic_to_shared(probs_s) + threadIdx.x * lane_stride(nb);
-    if (b < c.blk[1]) decode_runs<V, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P);
-    else if (b < c.blk[2]) decode_runs<V, 2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P);
-    else decode_runs<V, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P);
+    // lane rings of coded bytes first, then the lane-private probability trees
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
+    const uint32_t R = base + threadIdx.x * kRingBytes;
+    const uint32_t P = base + kRPW * kRingBytes + threadIdx.x * lane_stride(nb);
+    if (b < c.blk[1]) decode_runs<V, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P, R);
+    else if (b < c.blk[2]) decode_runs<V, 2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P, R);
+    else decode_runs<V, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R);
 }
 
 void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
@@ -642,10 +811,13 @@ void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n
         if (c.n[k] > 0) nbmax = 1 << k;
     }
     if (c.blk[3] == 0) return;
-    const size_t smem = (size_t)lane_stride(nbmax) * kRPW;
+    const size_t smem = (size_t)(lane_stride(nbmax) + kRingBytes) * kRPW;
     const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
-    const int v = ev ? atoi(ev) : 3;
-    if (v == 3) {
+    const int v = ev ? atoi(ev) : 4;
+    if (v == 4) {
+        cudaFuncSetAttribute(rc_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rc_decode_kernel<4><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+    } else if (v == 3) {
         cudaFuncSetAttribute(rc_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         rc_decode_kernel<3><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
     } else if (v == 1) {

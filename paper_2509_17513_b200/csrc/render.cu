@@ -31,7 +31,7 @@ void launch_project_soa(const SoaSrc& src, const CamDev& cam, RenderWork* w, int
 
 enum { C_NVIS = 0, C_NKEYS = 1, C_DMIN = 2, C_DMAX = 3, C_OVF = 4, C_N = 5, C_KCLAMP = 6,
        C_RN = 7, C_NPASS = 8 /* int pair: passes, key shift */, C_MAXK = 9 /* sticky */,
-       C_TOTK = 10, C_EMITK = 11, C_LONGRUNS = 12 };
+       C_TOTK = 10, C_EMITK = 11, C_LONGRUNS = 12, C_TIETICKET = 13 };
 
 CamDev make_cam(const gsv_camera& c) {
     CamDev d;
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256) reset_frame_kernel(unsigned long long* ct
     ctr[C_TOTK] = 0;
     ctr[C_EMITK] = 0;
     ctr[C_LONGRUNS] = 0;
+    ctr[C_TIETICKET] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[0] = 0;
     reinterpret_cast<int*>(ctr + C_NPASS)[1] = 0;
 }
@@ -139,10 +140,18 @@ __global__ void __launch_bounds__(256) depth_key_prep(uint64_t* __restrict__ ful
 // depths sharing one truncated key, e.g. a far outlier stretching the depth
 // range -- are listed for depth_tie_long (a CTA per run).
 constexpr uint32_t kShortTieRun = 32;
-__global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t* __restrict__ k1,
-                                uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
-                                const uint64_t* __restrict__ full, unsigned long long* __restrict__ ctr,
-                                uint32_t* __restrict__ long_runs) {
+__device__ void tie_sort_long_runs(uint32_t* __restrict__ idx, const uint64_t* __restrict__ full, uint32_t nruns,
+                                   const uint32_t* __restrict__ long_runs, uint64_t* __restrict__ sk0,
+                                   uint32_t* __restrict__ si0, uint64_t* __restrict__ sk1,
+                                   uint32_t* __restrict__ si1);
+
+__global__ void __launch_bounds__(256) depth_tie_fixup(const uint32_t* __restrict__ k0,
+                                                       const uint32_t* __restrict__ k1, uint32_t* __restrict__ i0,
+                                                       uint32_t* __restrict__ i1, const uint64_t* __restrict__ full,
+                                                       unsigned long long* __restrict__ ctr,
+                                                       uint32_t* __restrict__ long_runs, uint64_t* __restrict__ sk0,
+                                                       uint32_t* __restrict__ si0, uint64_t* __restrict__ sk1,
+                                                       uint32_t* __restrict__ si1) {
     const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
     const int shift = reinterpret_cast<const int*>(ctr + C_NPASS)[1];
     if (shift == 0 || np == 0) return;
@@ -187,6 +196,20 @@ __global__ void depth_tie_fixup(const uint32_t* __restrict__ k0, const uint32_t*
             idx[p] = v;
         }
     }
+    // the last CTA to finish sorts the listed long runs (rare: only when many
+    // distinct depths share a truncated key); no extra launch per frame
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long t = atomicAdd(ctr + C_TIETICKET, 1ull);
+        last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t nruns = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(ctr + C_LONGRUNS);
+    if (nruns) tie_sort_long_runs(idx, full, nruns, long_runs, sk0, si0, sk1, si1);
 }
 
 // (full key, index) order
@@ -198,18 +221,13 @@ __device__ __forceinline__ bool tie_less(uint64_t ka, uint32_t ia, uint64_t kb, 
 // bitonic in shared memory per chunk of kTieChunk, then merge passes between
 // two global scratch buffers (merge path per thread) for longer runs.
 constexpr int kTieThreads = 256, kTieChunk = 2048;
-__global__ void __launch_bounds__(kTieThreads) depth_tie_long(uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
-                                                               const uint64_t* __restrict__ full,
-                                                               const unsigned long long* __restrict__ ctr,
-                                                               const uint32_t* __restrict__ long_runs,
-                                                               uint64_t* __restrict__ sk0, uint32_t* __restrict__ si0,
-                                                               uint64_t* __restrict__ sk1, uint32_t* __restrict__ si1) {
+__device__ void tie_sort_long_runs(uint32_t* __restrict__ idx, const uint64_t* __restrict__ full, uint32_t nruns,
+                                   const uint32_t* __restrict__ long_runs, uint64_t* __restrict__ sk0,
+                                   uint32_t* __restrict__ si0, uint64_t* __restrict__ sk1,
+                                   uint32_t* __restrict__ si1) {
     __shared__ uint64_t ks[kTieChunk];
     __shared__ uint32_t is[kTieChunk];
-    const int np = reinterpret_cast<const int*>(ctr + C_NPASS)[0];
-    const uint32_t nruns = (uint32_t)ctr[C_LONGRUNS];
-    uint32_t* idx = (np & 1) ? i1 : i0;
-    for (uint32_t j = blockIdx.x; j < nruns; j += gridDim.x) {
+    for (uint32_t j = 0; j < nruns; j++) {
         const uint32_t r = long_runs[2 * j], e = long_runs[2 * j + 1], L = e - r;
         // 1) chunks of kTieChunk sorted in shared memory
         for (uint32_t c0 = 0; c0 < L; c0 += kTieChunk) {
@@ -985,10 +1003,9 @@ static unsigned debug_skip() {
 
 // exact order among ties of the truncated depth key (2 launches)
 static void launch_tie_fixup(RenderWork* w, cudaStream_t s) {
-    depth_tie_fixup<<<148 * 4, 256, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0], w->ctr,
-                                             w->tie_runs);
-    depth_tie_long<<<148, kTieThreads, 0, s>>>(w->didx[0], w->didx[1], w->dkey[0], w->ctr, w->tie_runs, w->dkey[1],
-                                               w->tval[0], w->tie_k, w->tval[1]);
+    depth_tie_fixup<<<148 * 4, kTieThreads, 0, s>>>(w->tkey[0], w->tkey[1], w->didx[0], w->didx[1], w->dkey[0],
+                                                     w->ctr, w->tie_runs, w->dkey[1], w->tval[0], w->tie_k,
+                                                     w->tval[1]);
 }
 
 // Enqueue one frame.  `project` enqueues the projection kernel into w.
@@ -1025,7 +1042,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             radix_sort<uint32_t>(w->tkey, w->didx, ctr + C_N, w->cap_n, depth_key_bits() / 8, npass, sc.ghist, sc, s);
         launch_tie_fixup(w, s);
         if (dbl & 64) launch_tie_fixup(w, s);
-        count_launch(3 + radix_launches(depth_key_bits() / 8, true));
+        count_launch(2 + radix_launches(depth_key_bits() / 8, true));
     }
     prof_mark(ST_EMIT, s);
     std::vector<uint32_t> bounds;

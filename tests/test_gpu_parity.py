@@ -396,3 +396,29 @@ def test_truncated_coded_block_is_codec_error(gsvb, bits):
     d = json.loads((GOLDEN / "conformance" / "rc_u8_random.json").read_text())
     good, _ = gsvb.CodedPayload.from_bytes(base64.b64decode(d["payload_b64"]))
     assert gsvb.decode_planes(good)[0].samples.ravel().tolist() == d["expected_samples"][0]
+
+
+@pytest.mark.parametrize("variant", ["1", "2", "3", "4"])
+def test_range_decoder_variants_bit_exact(gsvb, variant, monkeypatch):
+    """Every range-decoder variant (GSV_RC_VARIANT: 1 C++ fast path, 2 PTX
+    step, 3 + zero-prefix test, 4 + saturated zero-prefix test, the default)
+    decodes the reference-encoded codec-1 containers to the oracle's integer
+    codes at every frame."""
+    monkeypatch.setenv("GSV_RC_VARIANT", variant)
+    for name in ("c1mini_rc", "s1_rc", "deg2_rc", "wide32_rc"):
+        data = container(name)
+        info = O.read_structure(data)
+        k = info.layer_count
+        deg = info.sh_degree
+        order = [("position", c) for c in range(3)] + [("rotation", c) for c in range(4)] + \
+            [("scales", c) for c in range(3)] + [("opacity", 0)] + \
+            [("sh", c) for c in range(3 * (deg + 1) ** 2)]
+        with gsvb.DeviceVideo(data, k) as v:
+            for t in range(v.frame_count):
+                gi = v.group_of(t)
+                vals = O.decode_group_codes(data, info, gi, k)
+                tl = t - info.groups[gi].start_frame
+                exp = np.concatenate([np.stack([vals[l][key][0][tl] for key in order], axis=1)
+                                      for l in range(k)])
+                got = v.frame_codes(t).cpu().numpy().astype(np.uint32)
+                assert np.array_equal(got, exp), (name, t)

@@ -133,8 +133,9 @@ def test_c2_codec1_codes_across_29_planes(gsvb, c2_group):
     cfg, blobs, _ = c2_group
     data = blobs[1]
     info, vals, _ = _oracle_frames(data, cfg.layers, [])
-    order = [(0, c) for c in range(3)] + [(1, c) for c in range(4)] + [(2, c) for c in range(3)] + \
-        [(3, 0)] + [(4, c) for c in range(3 * (info.sh_degree + 1) ** 2)]
+    order = [("position", c) for c in range(3)] + [("rotation", c) for c in range(4)] + \
+        [("scales", c) for c in range(3)] + [("opacity", 0)] + \
+        [("sh", c) for c in range(3 * (info.sh_degree + 1) ** 2)]
     rc_planes = 0
     with gsvb.DeviceVideo(data, cfg.layers) as v:
         assert v.frame_count == 30 and v.group_of(29) == 0
