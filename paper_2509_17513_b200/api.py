@@ -21,6 +21,7 @@ import math
 import os
 import tempfile
 import io
+import struct
 import threading
 from pathlib import Path
 from typing import Sequence
@@ -142,27 +143,43 @@ def _structure_from_bytes(data: bytes) -> ContainerInfo:
                          info.flags, tuple(groups))
 
 
+def _read_directory(f) -> bytes:
+    """Header + directory bytes from the current position of `f`, read the
+    way read_structure reads them (container.py:151-191): exactly the
+    header, then per group the fixed part and counts, per layer the channel
+    count and its entries -- never a byte past the directory (so a prefix
+    read touches no payload byte of a higher layer).  A short read returns
+    the truncated bytes; the native parser then raises the reference's
+    "unexpected end of container" for them."""
+    out = bytearray()
+
+    def take(n):
+        chunk = f.read(n)
+        out.extend(chunk)
+        return len(chunk) == n
+
+    if not take(42):
+        return bytes(out)
+    L, G = out[6], struct.unpack_from("<H", out, 8)[0]
+    if out[:4] != b"GSV1" or struct.unpack_from("<H", out, 4)[0] != 1 or L < 1:
+        return bytes(out)  # the parser raises the header's error, as the reference does
+    for _ in range(G):
+        if not take(8 + 4 * L):
+            return bytes(out)
+        for _ in range(L):
+            if not take(2):
+                return bytes(out)
+            if not take(28 * struct.unpack_from("<H", out, len(out) - 2)[0]):
+                return bytes(out)
+    return bytes(out)
+
+
 def _read_prefix(f, up_to_layer: int | None):
     """Read header + directory, then only the payload bytes of layers <= k
     (container.py:276-283): the returned buffer has zeros elsewhere, so no
     byte of a higher layer is ever read from `f`."""
-    start = f.tell()
-    head = f.read(42)
-    if len(head) < 42:
-        raise FormatError("unexpected end of container (wanted 42 bytes)")
-    # grow the directory read until the C parser is satisfied
-    want = 4096
-    while True:
-        f.seek(start)
-        blob = f.read(want)
-        try:
-            info = _structure_from_bytes(blob)
-            break
-        except FormatError as e:
-            if "unexpected end" in str(e) and len(blob) == want:
-                want *= 4
-                continue
-            raise
+    blob = _read_directory(f)
+    info = _structure_from_bytes(blob)
     k = info.layer_count if up_to_layer is None else up_to_layer
     if not 1 <= k <= info.layer_count:
         raise InvalidInputError(f"layer {up_to_layer} out of range 1..{info.layer_count}")
@@ -170,8 +187,7 @@ def _read_prefix(f, up_to_layer: int | None):
     # entry.offset, container.py:282) while the header and directory come
     # from the current position, as read_structure reads them
     L = info.layer_count
-    hdr = 42 + sum(8 + 4 * L + sum(2 + 28 * len(g.channels[l]) for l in range(L)) for g in info.groups)
-    buf = bytearray(blob[:hdr])  # header + directory only (no payload bytes of any layer yet)
+    buf = bytearray(blob)  # header + directory only (no payload bytes of any layer yet)
     for g in info.groups:
         for l in range(k):
             for e in g.channels[l]:
@@ -196,19 +212,7 @@ def read_structure(f) -> ContainerInfo:
     """read_structure (container.py:151-191) for a binary file object or bytes."""
     if isinstance(f, (bytes, bytearray, memoryview)):
         return _structure_from_bytes(bytes(f))
-    start = f.tell()
-    want = 4096
-    while True:
-        f.seek(start)
-        blob = f.read(want)
-        try:
-            info = _structure_from_bytes(blob)
-        except FormatError as e:
-            if "unexpected end" in str(e) and len(blob) == want:
-                want *= 4
-                continue
-            raise
-        return info
+    return _structure_from_bytes(_read_directory(f))
 
 
 def read_container_info(path) -> ContainerInfo:

@@ -285,11 +285,13 @@ struct RunSet {
     std::vector<PlaneRef> planes;  // device addresses
     DevBuf d_runs, d_planes, d_planebuf, d_rc, d_chunk, d_crc, d_jobs;
     std::vector<uint32_t> crc;     // computed CRC per run
+    std::vector<uint32_t> key;     // channel (attribute << 8 | component) per run: decode order
 
     // planes of `pr` (blob-relative) -> device addresses at dev_blob; RC outputs
     // are assigned later by finalize().
-    void add(ParsedRun& pr, const uint8_t* dev_blob) {
+    void add(ParsedRun& pr, const uint8_t* dev_blob, uint32_t chan = 0) {
         RunDesc r = pr.rd;
+        key.push_back(chan);
         r.plane_base = (uint32_t)planes.size();
         const uint32_t run_id = (uint32_t)runs.size();
         for (auto p : pr.planes) {
@@ -330,6 +332,12 @@ struct RunSet {
             const int nb = runs[i].bits / 8;
             rc_runs[nb == 1 ? 0 : (nb == 2 ? 1 : 2)].push_back((uint32_t)i);
         }
+        // lanes of a decoder warp run in lock-step: runs of one channel
+        // (same statistics, same fast/slow paths) share warps
+        const char* eo = getenv("GSV_RC_ORDER");
+        if (!eo || atoi(eo) != 0)
+            for (auto& v : rc_runs)
+                std::stable_sort(v.begin(), v.end(), [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
         std::vector<uint32_t> rc_all;
         for (int b = 0; b < 3; b++) rc_all.insert(rc_all.end(), rc_runs[b].begin(), rc_runs[b].end());
         std::vector<uint32_t> chunk_prefix(planes.size() + 1, 0);
@@ -502,7 +510,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                     break;
                 }
                 const int run_id = (int)v->runs.runs.size();
-                v->runs.add(pr, dev_addr(g, e.offset));
+                v->runs.add(pr, dev_addr(g, e.offset), (uint32_t)e.attr << 8 | e.comp);
                 run_order.push_back(o);
                 run_name.push_back(nm);
                 if (pr.rd.count != gd.frame_count) {

@@ -24,6 +24,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "gsv_internal.h"
 
 namespace gsv {
@@ -32,6 +34,9 @@ constexpr int kRPW = 32;  // runs per warp
 
 // dev statistics: bytes redone on the careful path
 __device__ unsigned long long g_rc_slow_bytes;
+// dev profile (tools/rc_time.py): when set, per decoded run (run id, clock64
+// cycles from the run's first plane to its last), indexed like rc_runs
+__device__ unsigned long long* g_rc_prof;
 
 __global__ void copy_planes_kernel(const CopyJob* __restrict__ jobs, int njobs) {
     for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
@@ -746,6 +751,441 @@ __device__ __forceinline__ void decode_plane(uint32_t P, uint32_t R, const Plane
     }
 }
 
+// ===========================================================================
+// Variant 5: warp-cooperative speculative decoding.
+//
+// The serial chain of one run is what bounds codec 1 (a run's decisions
+// depend on each other; runs are the only independent units), and a lane
+// that walks the tree alone spends ~25 instructions per decision on one
+// sub-partition.  Here the LANES of a warp share ONE run and decode a byte by
+// speculation over its leading decisions: lane i assumes the byte starts
+// with the bits of i and evaluates those decisions along its own path --
+// bound, interval update, renormalisation; the bit is known, so the compare
+// is only a check off the chain -- and the one lane whose assumed bits are
+// the decisions the reference makes (at its first wrong bit a lane's state is
+// still the true state, so its check fails there) holds the true state.  A
+// ballot finds it and a shuffle hands its state to every lane.  The bit tree
+// lives in REGISTERS distributed over the lanes: a lane keeps the nodes of
+// its assumed path (shared nodes replicated in every lane whose path crosses
+// them) and, below it, its own subtree; after each byte every lane adapts the
+// copies it holds of the winner's path, so no probability goes through
+// shared memory on the chain.  The tree is only written to shared memory when
+// a byte needs the careful path (a 16-bit renormalisation or more than four
+// stream bytes in one byte: the byte is redone there by the scalar decoder).
+//   * 16-bit runs (position residuals: the longest chains): one run per warp,
+//     low byte = 5 assumed bits (32 lanes) + 3 decisions each lane takes in
+//     its own subtree; high byte (always zero here) by the saturated zero test
+//     of variant 4, else the same speculation on its tree.
+//   * 8-bit runs (residuals below 16): two runs per warp, 16 lanes each: the
+//     saturated zero nibble (p = 4081 on nodes 1, 2, 4, 8) followed by 4
+//     assumed bits of the low nibble; any other byte (nibble not zero, zero
+//     path not saturated) takes the careful path.
+// Same arithmetic, same stream bytes, same adaptation as _rc.py:121-155.
+
+// p + ((K - p) >> 4) for a bit known as a u32 0/1 (see adapt())
+__device__ __forceinline__ uint32_t adapt_u(uint32_t p, uint32_t bit) {
+    return p + (uint32_t)(((int32_t)(bit ? 15u : 4096u) - (int32_t)p) >> 4);
+}
+
+// Known-bit decision: km = 0xFFFFFFFF when the assumed bit is 1, else 0;
+// pk = km ? -p : p and rm = r & km (so rr = a * pk + rm is bit ? r - b : b in
+// one multiply-add).  Produces rm for the next step (mask kmn) beside a.
+__device__ __forceinline__ void kstep(uint32_t& a, uint32_t& rm, uint32_t& c, uint32_t& sel, uint32_t& rmin,
+                                      uint32_t& bad, uint32_t& rr, uint32_t p, uint32_t pk, uint32_t km,
+                                      uint32_t kmn, uint32_t bhi) {
+    asm("{\n\t"
+        ".reg .pred pl, pk1;\n\t"
+        ".reg .u32 b, t, t4, t12, t8, m0, m1;\n\t"
+        "mul.lo.u32 b, %0, %8;\n\t"
+        "mad.lo.u32 %6, %0, %9, %1;\n\t"
+        "set.ge.u32.u32 t, %2, b;\n\t"
+        "xor.b32 t, t, %10;\n\t"
+        "or.b32 %5, %5, t;\n\t"
+        "setp.ne.u32 pk1, %10, 0;\n\t"
+        "@pk1 sub.u32 %2, %2, b;\n\t"
+        "min.u32 %4, %4, %6;\n\t"
+        "setp.lt.u32 pl, %6, 16777216;\n\t"
+        "shr.u32 t4, %6, 4;\n\t"
+        "shr.u32 t12, %6, 12;\n\t"
+        "selp.u32 %0, t4, t12, pl;\n\t"
+        "shl.b32 t8, %6, 8;\n\t"
+        "and.b32 m1, t8, %11;\n\t"
+        "and.b32 m0, %6, %11;\n\t"
+        "selp.u32 %1, m1, m0, pl;\n\t"
+        "@pl mov.u32 %6, t8;\n\t"
+        "@pl prmt.b32 %2, %2, %7, %3;\n\t"
+        "@pl sub.u32 %3, %3, 1;\n\t"
+        "}"
+        : "+r"(a), "+r"(rm), "+r"(c), "+r"(sel), "+r"(rmin), "+r"(bad), "=r"(rr)
+        : "r"(bhi), "r"(p), "r"(pk), "r"(km), "r"(kmn));
+}
+
+// Full decision (the bit is decided here): as rc_step, without the node walk.
+__device__ __forceinline__ uint32_t fstep(uint32_t& a, uint32_t& r, uint32_t& c, uint32_t& sel, uint32_t& rmin,
+                                          uint32_t& pn, uint32_t p, uint32_t bhi) {
+    uint32_t bitv;
+    asm("{\n\t"
+        ".reg .pred pb, pl;\n\t"
+        ".reg .u32 b, r1, rr, t4, t12, K, d;\n\t"
+        "mul.lo.u32 b, %0, %7;\n\t"
+        "setp.ge.u32 pb, %2, b;\n\t"
+        "sub.u32 r1, %1, b;\n\t"
+        "selp.u32 rr, r1, b, pb;\n\t"
+        "@pb sub.u32 %2, %2, b;\n\t"
+        "min.u32 %4, %4, rr;\n\t"
+        "setp.lt.u32 pl, rr, 16777216;\n\t"
+        "shr.u32 t4, rr, 4;\n\t"
+        "shr.u32 t12, rr, 12;\n\t"
+        "selp.u32 %0, t4, t12, pl;\n\t"
+        "@pl shl.b32 rr, rr, 8;\n\t"
+        "mov.u32 %1, rr;\n\t"
+        "@pl prmt.b32 %2, %2, %8, %3;\n\t"
+        "@pl sub.u32 %3, %3, 1;\n\t"
+        "selp.u32 K, 15, 4096, pb;\n\t"
+        "sub.s32 d, K, %7;\n\t"
+        "shr.s32 d, d, 4;\n\t"
+        "add.u32 %5, %7, d;\n\t"
+        "selp.u32 %6, 1, 0, pb;\n\t"
+        "}"
+        : "+r"(a), "+r"(r), "+r"(c), "+r"(sel), "+r"(rmin), "=r"(pn), "=r"(bitv)
+        : "r"(p), "r"(bhi));
+    return bitv;
+}
+
+// Zero decision at the saturated probability 4081 (kstep with bit 0, p fixed).
+__device__ __forceinline__ void zstep(uint32_t& a, uint32_t& r, uint32_t& c, uint32_t& sel, uint32_t& rmin,
+                                      uint32_t& bad, uint32_t bhi) {
+    asm("{\n\t"
+        ".reg .pred pl;\n\t"
+        ".reg .u32 b, t, t4, t12;\n\t"
+        "mul.lo.u32 b, %0, 4081;\n\t"
+        "set.ge.u32.u32 t, %2, b;\n\t"
+        "or.b32 %5, %5, t;\n\t"
+        "min.u32 %4, %4, b;\n\t"
+        "setp.lt.u32 pl, b, 16777216;\n\t"
+        "shr.u32 t4, b, 4;\n\t"
+        "shr.u32 t12, b, 12;\n\t"
+        "selp.u32 %0, t4, t12, pl;\n\t"
+        "@pl shl.b32 b, b, 8;\n\t"
+        "mov.u32 %1, b;\n\t"
+        "@pl prmt.b32 %2, %2, %6, %3;\n\t"
+        "@pl sub.u32 %3, %3, 1;\n\t"
+        "}"
+        : "+r"(a), "+r"(r), "+r"(c), "+r"(sel), "+r"(rmin), "+r"(bad)
+        : "r"(bhi));
+}
+
+// One bit tree over 32 lanes: p[d] = node (1 << d) | (lane >> (5 - d)) (the
+// lane's 5-bit path), s[0] = node 32 + lane, s[1 + b] = node 64 + 2 lane + b,
+// s[3 + q] = node 128 + 4 lane + q (the lane's subtree).
+struct Tree32 {
+    uint32_t p[5], s[7];
+};
+
+__device__ __forceinline__ void tree32_load(Tree32& t, uint32_t T, uint32_t lane) {
+#pragma unroll
+    for (int d = 0; d < 5; d++) t.p[d] = lds_u32(T + 4u * ((1u << d) | (lane >> (5 - d))));
+    t.s[0] = lds_u32(T + 4u * (32u + lane));
+#pragma unroll
+    for (int b = 0; b < 2; b++) t.s[1 + b] = lds_u32(T + 4u * (64u + 2u * lane + b));
+#pragma unroll
+    for (int q = 0; q < 4; q++) t.s[3 + q] = lds_u32(T + 4u * (128u + 4u * lane + q));
+}
+__device__ __forceinline__ void tree32_store(const Tree32& t, uint32_t T, uint32_t lane) {
+#pragma unroll
+    for (int d = 0; d < 5; d++) sts_u32(T + 4u * ((1u << d) | (lane >> (5 - d))), t.p[d]);
+    sts_u32(T + 4u * (32u + lane), t.s[0]);
+#pragma unroll
+    for (int b = 0; b < 2; b++) sts_u32(T + 4u * (64u + 2u * lane + b), t.s[1 + b]);
+#pragma unroll
+    for (int q = 0; q < 4; q++) sts_u32(T + 4u * (128u + 4u * lane + q), t.s[3 + q]);
+}
+// all 8 zero-path nodes at the fixed point (lane 0 holds them all)
+__device__ __forceinline__ bool tree32_zero_sat(const Tree32& t) {
+    bool all = t.s[0] == kZeroSat && t.s[1] == kZeroSat && t.s[3] == kZeroSat;
+#pragma unroll
+    for (int d = 0; d < 5; d++) all = all && t.p[d] == kZeroSat;
+    return __shfl_sync(0xFFFFFFFFu, all ? 1 : 0, 0) != 0;
+}
+
+// The careful path of a speculative byte: the tree goes to shared memory
+// (every lane writes the nodes it holds), the byte is decoded there by the
+// scalar careful decoder (every lane redundantly, identical state and
+// identical stores), and the lanes reload their nodes.
+__device__ __forceinline__ uint32_t careful32(Tree32& t, uint32_t T, uint32_t lane, uint32_t& rng, uint32_t& code,
+                                          CodedStream& cs) {
+    tree32_store(t, T, lane);
+    __syncwarp();
+    uint4 q0 = lds_quad(T);
+    const uint32_t v = decode_byte_slow(T, T, q0, rng, code, cs);
+    __syncwarp();
+    tree32_load(t, T, lane);
+    return v;
+}
+
+// One byte on a 32-lane tree: 5 assumed bits, 3 decisions in the lane's
+// subtree, the winner's state to every lane, copies of its path adapted.
+__device__ __forceinline__ uint32_t spec_byte32(Tree32& t, uint32_t T, uint32_t lane, uint32_t& rng, uint32_t& code,
+                                                CodedStream& cs) {
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t km[5], pk[5];
+#pragma unroll
+    for (int d = 0; d < 5; d++) {
+        km[d] = 0u - ((lane >> (4 - d)) & 1u);
+        pk[d] = km[d] ? 0u - t.p[d] : t.p[d];
+    }
+    uint32_t a = rng >> 12, rm = rng & km[0], c = code, sel = 0x2107u, rmin = 0xFFFFFFFFu, bad = 0, rr = 0;
+#pragma unroll
+    for (int d = 0; d < 5; d++) kstep(a, rm, c, sel, rmin, bad, rr, t.p[d], pk[d], km[d], d < 4 ? km[d + 1] : 0u, bhi);
+    uint32_t r = rr, pn5, pn6, pn7;
+    const uint32_t b5 = fstep(a, r, c, sel, rmin, pn5, t.s[0], bhi);
+    const uint32_t b6 = fstep(a, r, c, sel, rmin, pn6, b5 ? t.s[2] : t.s[1], bhi);
+    const uint32_t p7 = b5 ? (b6 ? t.s[6] : t.s[5]) : (b6 ? t.s[4] : t.s[3]);
+    const uint32_t b7 = fstep(a, r, c, sel, rmin, pn7, p7, bhi);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, bad == 0);
+    const uint32_t w = __ffs(m) - 1;  // exactly one lane (see above); m == 0 cannot happen
+    const uint32_t packed = (lane << 3 | b5 << 2 | b6 << 1 | b7) | ((0x2107u - sel) << 8) | (rmin < (1u << 16) ? 1u << 16 : 0u);
+    const uint32_t nr = __shfl_sync(0xFFFFFFFFu, r, w);
+    const uint32_t nc = __shfl_sync(0xFFFFFFFFu, c, w);
+    const uint32_t pw = __shfl_sync(0xFFFFFFFFu, packed, w);
+    const uint32_t used = (pw >> 8) & 0xFFu;
+    if (m == 0 || (pw >> 16) != 0 || used > 4u) return careful32(t, T, lane, rng, code, cs);
+    rng = nr;
+    code = nc;
+#pragma unroll
+    for (int d = 0; d < 5; d++) {
+        const bool match = ((lane ^ w) >> (5 - d)) == 0;
+        if (match) t.p[d] = adapt_u(t.p[d], (w >> (4 - d)) & 1u);
+    }
+    if (lane == w) {
+        t.s[0] = pn5;
+        if (b5) t.s[2] = pn6;
+        else t.s[1] = pn6;
+        const uint32_t q = 2u * b5 + b6;
+        t.s[3] = q == 0 ? pn7 : t.s[3];
+        t.s[4] = q == 1 ? pn7 : t.s[4];
+        t.s[5] = q == 2 ? pn7 : t.s[5];
+        t.s[6] = q == 3 ? pn7 : t.s[6];
+    }
+    cs.bb <<= 8 * used;
+    cs.nbits -= (int32_t)(8 * used);
+    cs.refill();
+    return pw & 0xFFu;
+}
+
+// saturated whole-zero-byte test (zero_byte_sat without the quad load)
+__device__ __forceinline__ bool zero_byte_sat_nq(uint32_t& rng, uint32_t& code, CodedStream& cs) {
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t b = shr_opaque<12>(rng) * kZeroSat, bp = b;
+#pragma unroll
+    for (int k = 1; k < 8; k++) {
+        bp = b;
+        b = shr_opaque<12>(b) * kZeroSat;
+    }
+    if (!(bp >= (1u << 24) && code < b)) return false;
+    const uint32_t S = b < (1u << 24) ? 1u : 0u;
+    rng = S ? b << 8 : b;
+    code = S ? __byte_perm(code, bhi, 0x2107u) : code;
+    cs.bb <<= 8 * S;
+    cs.nbits -= (int32_t)(8 * S);
+    cs.refill();
+    return true;
+}
+
+// 16-bit runs: one run per warp.  Smem per warp: the coded-byte ring (64 B)
+// then tree 0 and tree 1 (1 KiB each, node n at +4n), used only by the
+// careful path.
+template <bool PREV>
+__device__ __forceinline__ void spec16_plane(Tree32& t0, Tree32& t1, bool& sat1, uint32_t T0, uint32_t T1,
+                                             uint32_t R, uint32_t lane, const PlaneRef& pr,
+                                             const uint16_t* __restrict__ prev, uint16_t* __restrict__ out,
+                                             uint32_t hw, uint32_t w) {
+    CodedStream cs;
+    cs.init(pr.coded, pr.coded_len, R);
+    uint32_t code = cs.take32();
+    cs.refill();
+    uint32_t rng = 0xFFFFFFFFu;
+    uint32_t left = 0, above = 0, x = 0;
+    for (uint32_t base = 0; base < hw; base += 32) {
+        const uint32_t nb = min(32u, hw - base);
+        uint32_t pv = 0, slot = 0;
+        if (PREV && lane < nb) pv = prev[base + lane];
+#pragma unroll 1
+        for (uint32_t j = 0; j < nb; j++) {
+            const uint32_t lo = spec_byte32(t0, T0, lane, rng, code, cs);
+            uint32_t hi = 0;
+            if (!(sat1 && zero_byte_sat_nq(rng, code, cs))) {
+                hi = spec_byte32(t1, T1, lane, rng, code, cs);
+                sat1 = tree32_zero_sat(t1);
+            }
+            const uint32_t z = lo | hi << 8;
+            const uint32_t r = (z >> 1) ^ (0u - (z & 1u));
+            if (PREV) {
+                if (lane == j) slot = r;
+            } else {
+                const uint32_t idx = base + j;
+                const uint32_t pred = x > 0 ? left : (idx > 0 ? above : 0x8000u);
+                const uint32_t v = (pred + r) & 0xFFFFu;
+                if (x == 0) above = v;
+                left = v;
+                if (++x == w) x = 0;
+                if (lane == j) slot = v;
+            }
+        }
+        if (lane < nb) out[base + lane] = (uint16_t)(PREV ? pv + slot : slot);
+    }
+    cs.finish();
+}
+
+__device__ __forceinline__ void spec16_run(const RunDesc& r, const PlaneRef* __restrict__ planes, uint32_t T0,
+                                           uint32_t T1, uint32_t R, uint32_t lane) {
+    Tree32 t0, t1;
+#pragma unroll
+    for (int d = 0; d < 5; d++) {  // new_bittree_probs (_rc.py:304-317): zero-path nodes 3686
+        t0.p[d] = t1.p[d] = (lane >> (5 - d)) == 0 ? 3686u : 2048u;
+    }
+#pragma unroll
+    for (int k = 0; k < 7; k++) t0.s[k] = t1.s[k] = 2048u;
+    if (lane == 0) t0.s[0] = t0.s[1] = t0.s[3] = t1.s[0] = t1.s[1] = t1.s[3] = 3686u;
+    bool sat1 = false;
+    const uint32_t hw = (uint32_t)r.w * r.h;
+    for (int f = 0; f < r.count; f++) {
+        const PlaneRef pr = planes[r.plane_base + f];
+        if (pr.mode != 0) continue;  // RAW plane (already copied to aligned storage)
+        uint16_t* out = reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(pr.samples));
+        if (f > 0)
+            spec16_plane<true>(t0, t1, sat1, T0, T1, R, lane, pr,
+                               reinterpret_cast<const uint16_t*>(planes[r.plane_base + f - 1].samples), out, hw, r.w);
+        else
+            spec16_plane<false>(t0, t1, sat1, T0, T1, R, lane, pr, nullptr, out, hw, r.w);
+    }
+}
+
+// One tree over the 16 lanes h of a half warp, 8-bit runs: q[d] = node
+// (16 << d) | (h >> (4 - d)) (the low nibble's nodes on the lane's path; the
+// zero-path nodes 1, 2, 4, 8 sit at 4081 whenever the fast path runs).
+struct Tree16 {
+    uint32_t q[4];
+};
+__device__ __forceinline__ void tree16_load(Tree16& t, uint32_t T, uint32_t h) {
+#pragma unroll
+    for (int d = 0; d < 4; d++) t.q[d] = lds_u32(T + 4u * ((16u << d) | (h >> (4 - d))));
+}
+__device__ __forceinline__ bool tree16_sat(uint32_t T) {
+    return lds_u32(T + 4u) == kZeroSat && lds_u32(T + 8u) == kZeroSat && lds_u32(T + 16u) == kZeroSat &&
+           lds_u32(T + 32u) == kZeroSat;
+}
+
+__device__ __forceinline__ uint32_t careful16(Tree16& t, uint32_t T, uint32_t h, uint32_t hmask, uint32_t& rng,
+                                          uint32_t& code, CodedStream& cs, bool& sat) {
+#pragma unroll
+    for (int d = 0; d < 4; d++) sts_u32(T + 4u * ((16u << d) | (h >> (4 - d))), t.q[d]);
+    __syncwarp(hmask);
+    uint4 q0 = lds_quad(T);
+    const uint32_t v = decode_byte_slow(T, T, q0, rng, code, cs);
+    __syncwarp(hmask);
+    tree16_load(t, T, h);
+    sat = tree16_sat(T);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t spec_byte16(Tree16& t, uint32_t T, uint32_t h, uint32_t hmask, uint32_t& rng,
+                                                uint32_t& code, CodedStream& cs, bool& sat) {
+    if (!sat) return careful16(t, T, h, hmask, rng, code, cs, sat);
+    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+    uint32_t km[4], pk[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        km[d] = 0u - ((h >> (3 - d)) & 1u);
+        pk[d] = km[d] ? 0u - t.q[d] : t.q[d];
+    }
+    uint32_t a = rng >> 12, r = rng, c = code, sel = 0x2107u, rmin = 0xFFFFFFFFu, bad = 0, rr = 0;
+#pragma unroll
+    for (int d = 0; d < 4; d++) zstep(a, r, c, sel, rmin, bad, bhi);
+    uint32_t rm = r & km[0];
+#pragma unroll
+    for (int d = 0; d < 4; d++) kstep(a, rm, c, sel, rmin, bad, rr, t.q[d], pk[d], km[d], d < 3 ? km[d + 1] : 0u, bhi);
+    const uint32_t shift = (threadIdx.x & 16u);
+    const uint32_t m = (__ballot_sync(hmask, bad == 0) >> shift) & 0xFFFFu;
+    const uint32_t w = __ffs(m) - 1;
+    const uint32_t packed = h | ((0x2107u - sel) << 8) | (rmin < (1u << 16) ? 1u << 16 : 0u);
+    const uint32_t src = (w & 15u) | shift;
+    const uint32_t nr = __shfl_sync(hmask, rr, src);
+    const uint32_t nc = __shfl_sync(hmask, c, src);
+    const uint32_t pw = __shfl_sync(hmask, packed, src);
+    const uint32_t used = (pw >> 8) & 0xFFu;
+    if (m == 0 || (pw >> 16) != 0 || used > 4u) return careful16(t, T, h, hmask, rng, code, cs, sat);
+    rng = nr;
+    code = nc;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        const bool match = ((h ^ w) >> (4 - d)) == 0;
+        if (match) t.q[d] = adapt_u(t.q[d], (w >> (3 - d)) & 1u);
+    }
+    cs.bb <<= 8 * used;
+    cs.nbits -= (int32_t)(8 * used);
+    cs.refill();
+    return pw & 0xFu;
+}
+
+template <bool PREV>
+__device__ __forceinline__ void spec8_plane(Tree16& t, bool& sat, uint32_t T, uint32_t R, uint32_t h,
+                                            uint32_t hmask, const PlaneRef& pr, const uint8_t* __restrict__ prev,
+                                            uint8_t* __restrict__ out, uint32_t hw, uint32_t w) {
+    CodedStream cs;
+    cs.init(pr.coded, pr.coded_len, R);
+    uint32_t code = cs.take32();
+    cs.refill();
+    uint32_t rng = 0xFFFFFFFFu;
+    uint32_t left = 0, above = 0, x = 0;
+    for (uint32_t base = 0; base < hw; base += 16) {
+        const uint32_t nb = min(16u, hw - base);
+        uint32_t pv = 0, slot = 0;
+        if (PREV && h < nb) pv = prev[base + h];
+#pragma unroll 1
+        for (uint32_t j = 0; j < nb; j++) {
+            const uint32_t z = spec_byte16(t, T, h, hmask, rng, code, cs, sat);
+            const uint32_t r = (z >> 1) ^ (0u - (z & 1u));
+            if (PREV) {
+                if (h == j) slot = r;
+            } else {
+                const uint32_t idx = base + j;
+                const uint32_t pred = x > 0 ? left : (idx > 0 ? above : 0x80u);
+                const uint32_t v = (pred + r) & 0xFFu;
+                if (x == 0) above = v;
+                left = v;
+                if (++x == w) x = 0;
+                if (h == j) slot = v;
+            }
+        }
+        if (h < nb) out[base + h] = (uint8_t)(PREV ? pv + slot : slot);
+    }
+    cs.finish();
+}
+
+__device__ __forceinline__ void spec8_run(const RunDesc& r, const PlaneRef* __restrict__ planes, uint32_t T,
+                                          uint32_t R, uint32_t h, uint32_t hmask) {
+    // new_bittree_probs (_rc.py:304-317): the whole tree in shared memory
+    // (the careful path's home), the lane copies loaded from it
+    for (uint32_t i = h; i < 256; i += 16) sts_u32(T + 4u * i, (i != 0 && (i & (i - 1)) == 0) ? 3686u : 2048u);
+    __syncwarp(hmask);
+    Tree16 t;
+    tree16_load(t, T, h);
+    bool sat = false;
+    const uint32_t hw = (uint32_t)r.w * r.h;
+    for (int f = 0; f < r.count; f++) {
+        const PlaneRef pr = planes[r.plane_base + f];
+        if (pr.mode != 0) continue;
+        uint8_t* out = const_cast<uint8_t*>(pr.samples);
+        if (f > 0)
+            spec8_plane<true>(t, sat, T, R, h, hmask, pr, planes[r.plane_base + f - 1].samples, out, hw, r.w);
+        else
+            spec8_plane<false>(t, sat, T, R, h, hmask, pr, nullptr, out, hw, r.w);
+    }
+}
+
+constexpr uint32_t kSpecSmem = 2 * (kRingBytes + kTreeBytes);  // per block (2 u8 runs, or 1 u16 run with 2 trees)
+
 // One launch for every width class (no serialisation of the u8 and u16 runs
 // behind each other): blocks [0, nb1) decode the 8-bit runs, the next nb2
 // blocks the 16-bit runs, the rest the 32-bit runs.  One warp per CTA, so
@@ -753,13 +1193,14 @@ __device__ __forceinline__ void decode_plane(uint32_t P, uint32_t R, const Plane
 template <int V, int NB>
 __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, const uint32_t* __restrict__ rc_runs,
                                             int n, int blk, const PlaneRef* __restrict__ planes, uint32_t P,
-                                            uint32_t R) {
+                                            uint32_t R, int prof_base) {
     const int lane = threadIdx.x;
     for (int b = 0; b < NB; b++)  // new_bittree_probs (_rc.py:304-317)
         for (uint32_t i = 0; i < 256; i++)
             sts_u32(node_addr(P + b * kTreeBytes, i), (i != 0 && (i & (i - 1)) == 0) ? 3686u : 2048u);
-    const int gi = blk * kRPW + lane;
+    const int gi = blk * (int)blockDim.x + lane;
     if (gi >= n) return;
+    const long long t0 = clock64();
     const RunDesc r = runs[rc_runs[gi]];
     const uint32_t hw = (uint32_t)r.w * r.h;
     bool sat = false;  // variant 4: zero-path probabilities saturated (persists with the model)
@@ -774,6 +1215,10 @@ __device__ __forceinline__ void decode_runs(const RunDesc* __restrict__ runs, co
             decode_plane<V, NB, false>(P, R, pr, nullptr, out, hw, r.w, sat);
         }
     }
+    if (unsigned long long* prof = g_rc_prof) {
+        prof[2 * (prof_base + gi)] = rc_runs[gi];
+        prof[2 * (prof_base + gi) + 1] = (unsigned long long)(clock64() - t0);
+    }
 }
 
 struct RcClasses {
@@ -783,53 +1228,103 @@ struct RcClasses {
 };
 
 template <int V>
-__global__ void __launch_bounds__(kRPW) rc_decode_kernel(const RunDesc* __restrict__ runs,
+__global__ void __launch_bounds__(32) rc_decode_kernel(const RunDesc* __restrict__ runs,
                                                          const uint32_t* __restrict__ rc_runs, RcClasses c,
                                                          const PlaneRef* __restrict__ planes) {
     extern __shared__ uint4 probs_s[];
     const int b = blockIdx.x;
+    if (V == 5 && b < c.blk[2]) {
+        // variant 5: blocks [0, blk1): two 8-bit runs each; [blk1, blk2): one 16-bit run each
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
+        const uint32_t lane = threadIdx.x;
+        const long long t0 = clock64();
+        int gi;
+        if (b < c.blk[1]) {
+            const uint32_t half = lane >> 4, h = lane & 15u, hmask = 0xFFFFu << (16 * half);
+            gi = 2 * b + (int)half;
+            if (gi >= c.n[0]) return;
+            const uint32_t R = base + half * (kRingBytes + kTreeBytes);
+            spec8_run(runs[rc_runs[c.off[0] + gi]], planes, R + kRingBytes, R, h, hmask);
+            gi += c.off[0];
+            if (h != 0) return;
+        } else {
+            gi = b - c.blk[1];
+            spec16_run(runs[rc_runs[c.off[1] + gi]], planes, base + kRingBytes, base + kRingBytes + kTreeBytes, base,
+                       lane);
+            gi += c.off[1];
+            if (lane != 0) return;
+        }
+        if (unsigned long long* prof = g_rc_prof) {
+            prof[2 * gi] = rc_runs[gi];
+            prof[2 * gi + 1] = (unsigned long long)(clock64() - t0);
+        }
+        return;
+    }
     const int nb = b < c.blk[1] ? 1 : (b < c.blk[2] ? 2 : 4);
+    if constexpr (V == 5) {  // 32-bit runs: the lane-per-run decoder (variant 4)
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
+        const uint32_t R = base + threadIdx.x * kRingBytes;
+        const uint32_t P = base + blockDim.x * kRingBytes + threadIdx.x * lane_stride(4);
+        decode_runs<4, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R, c.off[2]);
+    } else {
     // lane rings of coded bytes first, then the lane-private probability trees
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
     const uint32_t R = base + threadIdx.x * kRingBytes;
-    const uint32_t P = base + kRPW * kRingBytes + threadIdx.x * lane_stride(nb);
-    if (b < c.blk[1]) decode_runs<V, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P, R);
-    else if (b < c.blk[2]) decode_runs<V, 2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P, R);
-    else decode_runs<V, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R);
+    const uint32_t P = base + blockDim.x * kRingBytes + threadIdx.x * lane_stride(nb);
+    if (b < c.blk[1]) decode_runs<V, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P, R, c.off[0]);
+    else if (b < c.blk[2])
+        decode_runs<V, 2>(runs, rc_runs + c.off[1], c.n[1], b - c.blk[1], planes, P, R, c.off[1]);
+    else decode_runs<V, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R, c.off[2]);
+    }
 }
 
 void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
                       const PlaneRef* planes, cudaStream_t s) {
     RcClasses c;
     int nbmax = 0, off = 0;
+    const char* er = getenv("GSV_RC_RPW");  // runs per warp (dev tuning)
+    int rpw = er ? atoi(er) : kRPW;
+    rpw = rpw < 1 ? 1 : (rpw > 32 ? 32 : rpw);
+    const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
+    const int v = ev ? atoi(ev) : 5;
     c.blk[0] = 0;
     for (int k = 0; k < 3; k++) {
         c.n[k] = n_per_class[k];
         c.off[k] = off;
         off += c.n[k];
-        c.blk[k + 1] = c.blk[k] + (c.n[k] + kRPW - 1) / kRPW;
+        // variant 5: 2 runs per block (8-bit), 1 (16-bit); 32-bit runs rpw per block
+        const int per = v == 5 ? (k == 0 ? 2 : (k == 1 ? 1 : 32)) : rpw;
+        c.blk[k + 1] = c.blk[k] + (c.n[k] + per - 1) / per;
         if (c.n[k] > 0) nbmax = 1 << k;
     }
     if (c.blk[3] == 0) return;
-    const size_t smem = (size_t)(lane_stride(nbmax) + kRingBytes) * kRPW;
-    const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
-    const int v = ev ? atoi(ev) : 4;
-    if (v == 4) {
+    size_t smem = (size_t)(lane_stride(nbmax) + kRingBytes) * rpw;
+    if (v == 5) {
+        smem = kSpecSmem;
+        if (c.n[2] > 0) smem = std::max(smem, (size_t)(lane_stride(4) + kRingBytes) * 32);
+        cudaFuncSetAttribute(rc_decode_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rc_decode_kernel<5><<<c.blk[3], 32, smem, s>>>(runs, rc_runs, c, planes);
+    } else if (v == 4) {
         cudaFuncSetAttribute(rc_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<4><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+        rc_decode_kernel<4><<<c.blk[3], rpw, smem, s>>>(runs, rc_runs, c, planes);
     } else if (v == 3) {
         cudaFuncSetAttribute(rc_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<3><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+        rc_decode_kernel<3><<<c.blk[3], rpw, smem, s>>>(runs, rc_runs, c, planes);
     } else if (v == 1) {
         cudaFuncSetAttribute(rc_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<1><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+        rc_decode_kernel<1><<<c.blk[3], rpw, smem, s>>>(runs, rc_runs, c, planes);
     } else {
         cudaFuncSetAttribute(rc_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<2><<<c.blk[3], kRPW, smem, s>>>(runs, rc_runs, c, planes);
+        rc_decode_kernel<2><<<c.blk[3], rpw, smem, s>>>(runs, rc_runs, c, planes);
     }
 }
 
 }  // namespace gsv
+
+// dev: per-run decode cycles into `buf` (2 x u64 per range-coded run), or off
+extern "C" int gsv_dev_rc_profile(unsigned long long* buf) {
+    return cudaMemcpyToSymbol(gsv::g_rc_prof, &buf, sizeof buf) == cudaSuccess ? 0 : -1;
+}
 
 extern "C" unsigned long long gsv_dev_rc_slow_bytes(int reset) {
     unsigned long long v = 0;

@@ -126,8 +126,9 @@ def c2_group(gsvb):
 
 
 def test_c2_codec1_codes_across_29_planes(gsvb, c2_group):
-    """Codec 1 with the bench's 30-frame group: every run is 1 RAW keyframe
-    plane + 29 range-coded planes under one adaptive model; the integer
+    """Codec 1 with the bench's 30-frame group: runs of 29 or 30 range-coded
+    planes (a RAW keyframe plane when coding it does not pay) under one
+    adaptive model; the integer
     codes of frames 1, 15 and 29 (all 6 layers, all 23 channels) equal the
     oracle's decode (_rc.py:121-155, 282-301)."""
     cfg, blobs, _ = c2_group
@@ -136,7 +137,7 @@ def test_c2_codec1_codes_across_29_planes(gsvb, c2_group):
     order = [("position", c) for c in range(3)] + [("rotation", c) for c in range(4)] + \
         [("scales", c) for c in range(3)] + [("opacity", 0)] + \
         [("sh", c) for c in range(3 * (info.sh_degree + 1) ** 2)]
-    rc_planes = 0
+    rc_planes = []
     with gsvb.DeviceVideo(data, cfg.layers) as v:
         assert v.frame_count == 30 and v.group_of(29) == 0
         for t in (1, 15, 29):
@@ -151,8 +152,8 @@ def test_c2_codec1_codes_across_29_planes(gsvb, c2_group):
                 blob = data[e.offset:e.offset + e.size]
                 if blob[0] == 1 and blob[14] == 0:  # codec 1, per-plane mode table
                     modes = blob[15:15 + 30]
-                    rc_planes = max(rc_planes, sum(1 for m in modes if m == 0))
-    assert rc_planes == 29
+                    rc_planes.append(sum(1 for m in modes if m == 0))
+    assert min(rc_planes) >= 29 and 29 in rc_planes and 30 in rc_planes
 
 
 @pytest.mark.parametrize("codec", [0, 1])
