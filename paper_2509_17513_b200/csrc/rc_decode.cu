@@ -908,26 +908,112 @@ __device__ __forceinline__ bool tree32_zero_sat(const Tree32& t) {
     return __shfl_sync(0xFFFFFFFFu, all ? 1 : 0, 0) != 0;
 }
 
-// The careful path of a speculative byte: the tree goes to shared memory
-// (every lane writes the nodes it holds), the byte is decoded there by the
-// scalar careful decoder (every lane redundantly, identical state and
-// identical stores), and the lanes reload their nodes.
+// The coded bytes of one plane as seen by the 32 lanes of a warp that share
+// one run (every lane holds the same state): a 64-bit big-endian buffer, the
+// next word to append, and the word after it loaded a step ahead (a
+// predicated broadcast load, so its latency is spent while other samples
+// decode).  A word is appended whenever 32 bits or fewer are buffered: one
+// append per sample keeps >= 32 bits buffered at a sample's start (the fast
+// path checks it has the bytes it takes).  Bytes at or past the block end
+// read as zero (_rc.py:129,150); loads are clamped inside the block.
+struct WarpStream {
+    const uint32_t* wb;  // 4-B aligned base (global)
+    int32_t wend;        // bytes from wb to the block end
+    int32_t wlast;       // last loadable word index (>= 0)
+    uint32_t k;          // word index (from wb) of nextw
+    uint32_t nextw;      // big-endian, masked
+    uint32_t pend;       // raw word k + 1
+    uint64_t bb;
+    int32_t nbits;
+
+    __device__ __forceinline__ const uint32_t* addr(uint32_t j) const {
+        return wb + min((int32_t)j, wlast);
+    }
+    __device__ __forceinline__ uint32_t be_masked(uint32_t raw, uint32_t j) const {
+        const int32_t vb = wend - 4 * (int32_t)j;  // valid bytes of word j
+        const uint32_t m = vb >= 4 ? 0xFFFFFFFFu : (vb > 0 ? (1u << (8 * vb)) - 1u : 0u);
+        return __byte_perm(raw & m, 0u, 0x0123);
+    }
+    __device__ __forceinline__ void init(const uint8_t* block, uint32_t len) {
+        const uintptr_t st = reinterpret_cast<uintptr_t>(block) + 1;  // byte 0 is always zero
+        const uintptr_t w0 = st & ~uintptr_t(3);
+        const uint32_t skip = (uint32_t)(st & 3);
+        wb = reinterpret_cast<const uint32_t*>(w0);
+        wend = (int32_t)((reinterpret_cast<uintptr_t>(block) + len) - w0);
+        wlast = max((wend - 1) >> 2, 0);
+        bb = (uint64_t)(be_masked(__ldg(addr(0)), 0) << (8 * skip)) << 32;
+        nbits = 32 - 8 * (int32_t)skip;
+        k = 1;
+        nextw = be_masked(__ldg(addr(1)), 1);
+        pend = __ldg(addr(2));
+        append();
+    }
+    __device__ __forceinline__ void append() {
+        const bool need = nbits <= 32;
+        const uint32_t sh = (uint32_t)(32 - nbits) & 63u;
+        bb |= need ? (uint64_t)nextw << sh : 0ull;
+        nbits += need ? 32 : 0;
+        k += need ? 1u : 0u;
+        const uint32_t nv = be_masked(pend, k);
+        nextw = need ? nv : nextw;
+        // the next word's load, predicated straight into `pend` (no select
+        // that would wait for it)
+        const uint32_t* ap = addr(k + 1);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.u32 %0, [%1];\n\t}"
+                     : "+r"(pend)
+                     : "l"(ap), "r"(need ? 1u : 0u));
+    }
+    __device__ __forceinline__ void consume(uint32_t nbytes) {  // nbytes <= 7
+        bb <<= 8 * nbytes;
+        nbits -= 8 * (int32_t)nbytes;
+    }
+    __device__ __forceinline__ uint32_t next_byte() {
+        const uint32_t v = (uint32_t)(bb >> 56);
+        consume(1);
+        append();
+        return v;
+    }
+};
+
+// The careful path: the tree goes to shared memory (every lane writes the
+// nodes it holds), the byte is decoded there one decision at a time exactly
+// as _rc.py:136-153 (every lane redundantly: identical state, identical
+// stores), and the lanes reload their nodes.
 __device__ __forceinline__ uint32_t careful32(Tree32& t, uint32_t T, uint32_t lane, uint32_t& rng, uint32_t& code,
-                                          CodedStream& cs) {
+                                          WarpStream& ws) {
     tree32_store(t, T, lane);
     __syncwarp();
-    uint4 q0 = lds_quad(T);
-    const uint32_t v = decode_byte_slow(T, T, q0, rng, code, cs);
+    atomicAdd(&g_rc_slow_bytes, 1ull);
+    uint32_t ctx = 1;
+    for (int k = 0; k < 8; k++) {
+        const uint32_t p = lds_u32(T + 4u * ctx);
+        const uint32_t bound = (rng >> 12) * p;
+        const bool bit = code >= bound;
+        code = bit ? code - bound : code;
+        rng = bit ? rng - bound : bound;
+        sts_u32(T + 4u * ctx, adapt(p, bit));
+        ctx = 2 * ctx + (bit ? 1u : 0u);
+        while (rng < (1u << 24)) {
+            code = (code << 8) | ws.next_byte();
+            rng <<= 8;
+        }
+    }
     __syncwarp();
     tree32_load(t, T, lane);
-    return v;
+    return ctx & 0xFFu;
 }
 
-// One byte on a 32-lane tree: 5 assumed bits, 3 decisions in the lane's
-// subtree, the winner's state to every lane, copies of its path adapted.
-__device__ __forceinline__ uint32_t spec_byte32(Tree32& t, uint32_t T, uint32_t lane, uint32_t& rng, uint32_t& code,
-                                                CodedStream& cs) {
-    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
+// Speculative evaluation of one byte on a 32-lane tree (nothing committed):
+// lane i assumes the 5 leading bits i, then takes 3 decisions in its own
+// subtree; the winner's interval state and a packed word (bit 31 valid, bit
+// 16 a 16-bit renormalisation seen, bits 8-15 stream bytes used, bits 0-7
+// the byte) reach every lane by OR-reductions (only the winner contributes).
+struct Spec32 {
+    uint32_t r, c, pw, pn5, pn6, pn7, b5, b6;
+};
+template <bool REDUX>
+__device__ __forceinline__ Spec32 spec32_eval(const Tree32& t, uint32_t lane, uint32_t rng, uint32_t code,
+                                              uint32_t bhi) {
     uint32_t km[5], pk[5];
 #pragma unroll
     for (int d = 0; d < 5; d++) {
@@ -937,108 +1023,169 @@ __device__ __forceinline__ uint32_t spec_byte32(Tree32& t, uint32_t T, uint32_t 
     uint32_t a = rng >> 12, rm = rng & km[0], c = code, sel = 0x2107u, rmin = 0xFFFFFFFFu, bad = 0, rr = 0;
 #pragma unroll
     for (int d = 0; d < 5; d++) kstep(a, rm, c, sel, rmin, bad, rr, t.p[d], pk[d], km[d], d < 4 ? km[d + 1] : 0u, bhi);
-    uint32_t r = rr, pn5, pn6, pn7;
-    const uint32_t b5 = fstep(a, r, c, sel, rmin, pn5, t.s[0], bhi);
-    const uint32_t b6 = fstep(a, r, c, sel, rmin, pn6, b5 ? t.s[2] : t.s[1], bhi);
-    const uint32_t p7 = b5 ? (b6 ? t.s[6] : t.s[5]) : (b6 ? t.s[4] : t.s[3]);
-    const uint32_t b7 = fstep(a, r, c, sel, rmin, pn7, p7, bhi);
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, bad == 0);
-    const uint32_t w = __ffs(m) - 1;  // exactly one lane (see above); m == 0 cannot happen
-    const uint32_t packed = (lane << 3 | b5 << 2 | b6 << 1 | b7) | ((0x2107u - sel) << 8) | (rmin < (1u << 16) ? 1u << 16 : 0u);
-    const uint32_t nr = __shfl_sync(0xFFFFFFFFu, r, w);
-    const uint32_t nc = __shfl_sync(0xFFFFFFFFu, c, w);
-    const uint32_t pw = __shfl_sync(0xFFFFFFFFu, packed, w);
-    const uint32_t used = (pw >> 8) & 0xFFu;
-    if (m == 0 || (pw >> 16) != 0 || used > 4u) return careful32(t, T, lane, rng, code, cs);
-    rng = nr;
-    code = nc;
+    Spec32 o;
+    uint32_t r = rr;
+    o.b5 = fstep(a, r, c, sel, rmin, o.pn5, t.s[0], bhi);
+    o.b6 = fstep(a, r, c, sel, rmin, o.pn6, o.b5 ? t.s[2] : t.s[1], bhi);
+    const uint32_t p7 = o.b5 ? (o.b6 ? t.s[6] : t.s[5]) : (o.b6 ? t.s[4] : t.s[3]);
+    const uint32_t b7 = fstep(a, r, c, sel, rmin, o.pn7, p7, bhi);
+    const bool ok = bad == 0;
+    const uint32_t packed = 0x80000000u | (rmin < (1u << 16) ? 1u << 16 : 0u) | ((0x2107u - sel) << 8) |
+                            (lane << 3) | (o.b5 << 2) | (o.b6 << 1) | b7;
+    if (REDUX) {
+        o.r = __reduce_or_sync(0xFFFFFFFFu, ok ? r : 0u);
+        o.c = __reduce_or_sync(0xFFFFFFFFu, ok ? c : 0u);
+        o.pw = __reduce_or_sync(0xFFFFFFFFu, ok ? packed : 0u);
+    } else {  // ballot, then the winner's registers by shuffles
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+        const uint32_t w = 31u - (uint32_t)__clz(m);
+        o.r = __shfl_sync(0xFFFFFFFFu, r, w);
+        o.c = __shfl_sync(0xFFFFFFFFu, c, w);
+        o.pw = __shfl_sync(0xFFFFFFFFu, packed, w);
+        o.pw = m ? o.pw : 0u;
+    }
+    return o;
+}
+// usable without the careful path: a winner, no 16-bit shift, <= 4 bytes
+__device__ __forceinline__ bool spec32_fast(uint32_t pw) {
+    return (pw >> 31) != 0u && (pw & 0x10000u) == 0u && ((pw >> 8) & 0xFFu) <= 4u;
+}
+// adapt every lane's copies of the winner's path (branch-free): a lane holds
+// the winner's depth-d node iff their top d bits agree (lane ^ w < 2^(5-d))
+__device__ __forceinline__ void spec32_commit(Tree32& t, const Spec32& o, uint32_t lane) {
+    const uint32_t w = (o.pw >> 3) & 31u;
+    const uint32_t x = lane ^ w;
 #pragma unroll
     for (int d = 0; d < 5; d++) {
-        const bool match = ((lane ^ w) >> (5 - d)) == 0;
-        if (match) t.p[d] = adapt_u(t.p[d], (w >> (4 - d)) & 1u);
+        const int32_t K = ((w >> (4 - d)) & 1u) ? 15 : 4096;  // warp-uniform
+        const uint32_t up = t.p[d] + (uint32_t)((K - (int32_t)t.p[d]) >> 4);
+        t.p[d] = x < (32u >> d) ? up : t.p[d];
     }
-    if (lane == w) {
-        t.s[0] = pn5;
-        if (b5) t.s[2] = pn6;
-        else t.s[1] = pn6;
-        const uint32_t q = 2u * b5 + b6;
-        t.s[3] = q == 0 ? pn7 : t.s[3];
-        t.s[4] = q == 1 ? pn7 : t.s[4];
-        t.s[5] = q == 2 ? pn7 : t.s[5];
-        t.s[6] = q == 3 ? pn7 : t.s[6];
-    }
-    cs.bb <<= 8 * used;
-    cs.nbits -= (int32_t)(8 * used);
-    cs.refill();
-    return pw & 0xFFu;
+    const bool iw = x == 0;
+    const uint32_t q = 2u * o.b5 + o.b6;
+    t.s[0] = iw ? o.pn5 : t.s[0];
+    t.s[1] = (iw && !o.b5) ? o.pn6 : t.s[1];
+    t.s[2] = (iw && o.b5) ? o.pn6 : t.s[2];
+    t.s[3] = (iw && q == 0) ? o.pn7 : t.s[3];
+    t.s[4] = (iw && q == 1) ? o.pn7 : t.s[4];
+    t.s[5] = (iw && q == 2) ? o.pn7 : t.s[5];
+    t.s[6] = (iw && q == 3) ? o.pn7 : t.s[6];
+}
+// one whole byte with its careful fallback (used off the fast path)
+template <bool REDUX>
+__device__ __forceinline__ uint32_t spec32_byte(Tree32& t, uint32_t T, uint32_t lane, uint32_t& rng, uint32_t& code,
+                                                WarpStream& ws) {
+    const Spec32 o = spec32_eval<REDUX>(t, lane, rng, code, (uint32_t)(ws.bb >> 32));
+    if (!spec32_fast(o.pw)) return careful32(t, T, lane, rng, code, ws);
+    spec32_commit(t, o, lane);
+    rng = o.r;
+    code = o.c;
+    ws.consume((o.pw >> 8) & 0xFFu);
+    ws.append();
+    return o.pw & 0xFFu;
 }
 
-// saturated whole-zero-byte test (zero_byte_sat without the quad load)
-__device__ __forceinline__ bool zero_byte_sat_nq(uint32_t& rng, uint32_t& code, CodedStream& cs) {
-    const uint32_t bhi = (uint32_t)(cs.bb >> 32);
-    uint32_t b = shr_opaque<12>(rng) * kZeroSat, bp = b;
+// The whole-zero-byte chain at the saturated probability: bounds b_k =
+// (b_{k-1} >> 12) * 4081, valid while no renormalisation comes before the
+// last decision (bp >= 2^24); the byte is zero iff code < b_8.
+struct ZeroTest {
+    uint32_t b, bp;
+};
+__device__ __forceinline__ ZeroTest zero_chain(uint32_t rng) {
+    ZeroTest z;
+    z.b = shr_opaque<12>(rng) * kZeroSat;
+    z.bp = z.b;
 #pragma unroll
     for (int k = 1; k < 8; k++) {
-        bp = b;
-        b = shr_opaque<12>(b) * kZeroSat;
+        z.bp = z.b;
+        z.b = shr_opaque<12>(z.b) * kZeroSat;
     }
-    if (!(bp >= (1u << 24) && code < b)) return false;
-    const uint32_t S = b < (1u << 24) ? 1u : 0u;
-    rng = S ? b << 8 : b;
-    code = S ? __byte_perm(code, bhi, 0x2107u) : code;
-    cs.bb <<= 8 * S;
-    cs.nbits -= (int32_t)(8 * S);
-    cs.refill();
-    return true;
+    return z;
 }
 
-// 16-bit runs: one run per warp.  Smem per warp: the coded-byte ring (64 B)
-// then tree 0 and tree 1 (1 KiB each, node n at +4n), used only by the
-// careful path.
-template <bool PREV>
+// 16-bit runs: one run per warp, the tree in registers over the lanes.  Per
+// sample the fast path is: the low byte by speculation, the high byte by the
+// saturated zero test on the winner's state, the commit -- one branch (to the
+// careful / general path) per sample.  Smem per warp: tree 0 and tree 1
+// (1 KiB each, node n at +4n), used only by the careful path.
+template <bool PREV, bool REDUX>
 __device__ __forceinline__ void spec16_plane(Tree32& t0, Tree32& t1, bool& sat1, uint32_t T0, uint32_t T1,
-                                             uint32_t R, uint32_t lane, const PlaneRef& pr,
-                                             const uint16_t* __restrict__ prev, uint16_t* __restrict__ out,
-                                             uint32_t hw, uint32_t w) {
-    CodedStream cs;
-    cs.init(pr.coded, pr.coded_len, R);
-    uint32_t code = cs.take32();
-    cs.refill();
+                                             uint32_t lane, const PlaneRef& pr, const uint16_t* __restrict__ prev,
+                                             uint16_t* __restrict__ out, uint32_t hw, uint32_t w) {
+    WarpStream ws;
+    ws.init(pr.coded, pr.coded_len);
+    uint32_t code = (uint32_t)(ws.bb >> 32);
+    ws.consume(4);
+    ws.append();
     uint32_t rng = 0xFFFFFFFFu;
     uint32_t left = 0, above = 0, x = 0;
     for (uint32_t base = 0; base < hw; base += 32) {
         const uint32_t nb = min(32u, hw - base);
         uint32_t pv = 0, slot = 0;
         if (PREV && lane < nb) pv = prev[base + lane];
-#pragma unroll 1
+#pragma unroll 2
         for (uint32_t j = 0; j < nb; j++) {
-            const uint32_t lo = spec_byte32(t0, T0, lane, rng, code, cs);
-            uint32_t hi = 0;
-            if (!(sat1 && zero_byte_sat_nq(rng, code, cs))) {
-                hi = spec_byte32(t1, T1, lane, rng, code, cs);
-                sat1 = tree32_zero_sat(t1);
+            const Spec32 o = spec32_eval<REDUX>(t0, lane, rng, code, (uint32_t)(ws.bb >> 32));
+            const uint32_t used = (o.pw >> 8) & 0xFFu;
+            const ZeroTest zt = zero_chain(o.r);
+            const uint32_t S = zt.b < (1u << 24) ? 1u : 0u;
+            const uint32_t nbyte = (uint32_t)(ws.bb >> (56 - 8 * (used & 7u))) & 0xFFu;
+            uint32_t z;
+            if (spec32_fast(o.pw) && sat1 && zt.bp >= (1u << 24) && o.c < zt.b &&
+                8 * (int32_t)(used + S) <= ws.nbits) {
+                spec32_commit(t0, o, lane);
+                rng = S ? zt.b << 8 : zt.b;
+                code = S ? (o.c << 8) | nbyte : o.c;
+                ws.consume(used + S);
+                ws.append();
+                z = o.pw & 0xFFu;
+            } else {  // rare: the careful low byte and/or the general high byte
+                uint32_t lo;
+                if (!spec32_fast(o.pw) || 8 * (int32_t)used > ws.nbits) {
+                    lo = careful32(t0, T0, lane, rng, code, ws);
+                } else {
+                    spec32_commit(t0, o, lane);
+                    rng = o.r;
+                    code = o.c;
+                    ws.consume(used);
+                    ws.append();
+                    ws.append();
+                    lo = o.pw & 0xFFu;
+                }
+                const ZeroTest z2 = zero_chain(rng);
+                uint32_t hi = 0;
+                if (sat1 && z2.bp >= (1u << 24) && code < z2.b) {
+                    const uint32_t S2 = z2.b < (1u << 24) ? 1u : 0u;
+                    rng = S2 ? z2.b << 8 : z2.b;
+                    code = S2 ? (code << 8) | (uint32_t)(ws.bb >> 56) : code;
+                    ws.consume(S2);
+                    ws.append();
+                } else {
+                    hi = spec32_byte<REDUX>(t1, T1, lane, rng, code, ws);
+                    sat1 = tree32_zero_sat(t1);
+                }
+                z = lo | hi << 8;
             }
-            const uint32_t z = lo | hi << 8;
             const uint32_t r = (z >> 1) ^ (0u - (z & 1u));
             if (PREV) {
-                if (lane == j) slot = r;
+                slot = lane == j ? r : slot;
             } else {
                 const uint32_t idx = base + j;
                 const uint32_t pred = x > 0 ? left : (idx > 0 ? above : 0x8000u);
                 const uint32_t v = (pred + r) & 0xFFFFu;
-                if (x == 0) above = v;
+                above = x == 0 ? v : above;
                 left = v;
-                if (++x == w) x = 0;
-                if (lane == j) slot = v;
+                x = x + 1 == w ? 0u : x + 1;
+                slot = lane == j ? v : slot;
             }
         }
         if (lane < nb) out[base + lane] = (uint16_t)(PREV ? pv + slot : slot);
     }
-    cs.finish();
 }
 
+template <bool REDUX>
 __device__ __forceinline__ void spec16_run(const RunDesc& r, const PlaneRef* __restrict__ planes, uint32_t T0,
-                                           uint32_t T1, uint32_t R, uint32_t lane) {
+                                           uint32_t T1, uint32_t lane) {
     Tree32 t0, t1;
 #pragma unroll
     for (int d = 0; d < 5; d++) {  // new_bittree_probs (_rc.py:304-317): zero-path nodes 3686
@@ -1054,10 +1201,10 @@ __device__ __forceinline__ void spec16_run(const RunDesc& r, const PlaneRef* __r
         if (pr.mode != 0) continue;  // RAW plane (already copied to aligned storage)
         uint16_t* out = reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(pr.samples));
         if (f > 0)
-            spec16_plane<true>(t0, t1, sat1, T0, T1, R, lane, pr,
+            spec16_plane<true, REDUX>(t0, t1, sat1, T0, T1, lane, pr,
                                reinterpret_cast<const uint16_t*>(planes[r.plane_base + f - 1].samples), out, hw, r.w);
         else
-            spec16_plane<false>(t0, t1, sat1, T0, T1, R, lane, pr, nullptr, out, hw, r.w);
+            spec16_plane<false, REDUX>(t0, t1, sat1, T0, T1, lane, pr, nullptr, out, hw, r.w);
     }
 }
 
@@ -1184,6 +1331,194 @@ __device__ __forceinline__ void spec8_run(const RunDesc& r, const PlaneRef* __re
     }
 }
 
+// ---------------------------------------------------------------------------
+// 8-bit runs, a lane per run (32 runs per warp in lock-step), branch-light:
+// the low-nibble subtree (15 nodes: 16, 32-33, 64-67, 128-135) lives in the
+// lane's REGISTERS; while the zero-path nodes 1, 2, 4, 8 sit at the fixed
+// point 4081 (8-bit residuals here never leave the low nibble) a byte is 4
+// zero decisions at p = 4081 + 4 decisions on the register subtree, the
+// probability of each taken from registers by selects prepared one decision
+// ahead, and the commit writes the 4 adapted nodes back by selects.  Any
+// other byte (a 1 in the top nibble, a 16-bit renormalisation, > 4 stream
+// bytes, the zero path not yet saturated) goes to the careful path on the
+// lane's shared-memory tree (the subtree is written there first and reloaded
+// after).  The stream is the WarpStream scheme per lane (the next word's
+// load predicated a step ahead).
+struct LaneStream {
+    const uint32_t* wb;
+    int32_t wend, wlast;
+    uint32_t k, nextw, pend;
+    uint64_t bb;
+    int32_t nbits;
+    __device__ __forceinline__ const uint32_t* addr(uint32_t j) const { return wb + min((int32_t)j, wlast); }
+    __device__ __forceinline__ uint32_t be_masked(uint32_t raw, uint32_t j) const {
+        const int32_t vb = wend - 4 * (int32_t)j;
+        const uint32_t m = vb >= 4 ? 0xFFFFFFFFu : (vb > 0 ? (1u << (8 * vb)) - 1u : 0u);
+        return __byte_perm(raw & m, 0u, 0x0123);
+    }
+    __device__ __forceinline__ void init(const uint8_t* block, uint32_t len) {
+        const uintptr_t st = reinterpret_cast<uintptr_t>(block) + 1;
+        const uintptr_t w0 = st & ~uintptr_t(3);
+        const uint32_t skip = (uint32_t)(st & 3);
+        wb = reinterpret_cast<const uint32_t*>(w0);
+        wend = (int32_t)((reinterpret_cast<uintptr_t>(block) + len) - w0);
+        wlast = max((wend - 1) >> 2, 0);
+        bb = (uint64_t)(be_masked(__ldg(addr(0)), 0) << (8 * skip)) << 32;
+        nbits = 32 - 8 * (int32_t)skip;
+        k = 1;
+        nextw = be_masked(__ldg(addr(1)), 1);
+        pend = __ldg(addr(2));
+        append();
+    }
+    __device__ __forceinline__ void append() {
+        const bool need = nbits <= 32;
+        const uint32_t sh = (uint32_t)(32 - nbits) & 63u;
+        bb |= need ? (uint64_t)nextw << sh : 0ull;
+        nbits += need ? 32 : 0;
+        k += need ? 1u : 0u;
+        const uint32_t nv = be_masked(pend, k);
+        nextw = need ? nv : nextw;
+        const uint32_t* ap = addr(k + 1);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.u32 %0, [%1];\n\t}"
+                     : "+r"(pend)
+                     : "l"(ap), "r"(need ? 1u : 0u));
+    }
+    __device__ __forceinline__ void consume(uint32_t nbytes) {
+        bb <<= 8 * nbytes;
+        nbits -= 8 * (int32_t)nbytes;
+    }
+    __device__ __forceinline__ uint32_t next_byte() {
+        const uint32_t v = (uint32_t)(bb >> 56);
+        consume(1);
+        append();
+        return v;
+    }
+};
+
+// subtree register index of node (16 << j) + q is (1 << j) - 1 + q
+__device__ __forceinline__ uint32_t nib_node(int i) {
+    return i == 0 ? 16u : (i < 3 ? 32u + (i - 1) : (i < 7 ? 64u + (i - 3) : 128u + (i - 7)));
+}
+
+__device__ __forceinline__ uint32_t lane8_careful(uint32_t (&n)[15], uint32_t T, uint32_t& rng, uint32_t& code,
+                                                  LaneStream& ls, bool& sat) {
+#pragma unroll
+    for (int i = 0; i < 15; i++) sts_u32(T + 4u * nib_node(i), n[i]);
+    atomicAdd(&g_rc_slow_bytes, 1ull);
+    uint32_t ctx = 1;
+    for (int k = 0; k < 8; k++) {
+        const uint32_t p = lds_u32(T + 4u * ctx);
+        const uint32_t bound = (rng >> 12) * p;
+        const bool bit = code >= bound;
+        code = bit ? code - bound : code;
+        rng = bit ? rng - bound : bound;
+        sts_u32(T + 4u * ctx, adapt(p, bit));
+        ctx = 2 * ctx + (bit ? 1u : 0u);
+        while (rng < (1u << 24)) {
+            code = (code << 8) | ls.next_byte();
+            rng <<= 8;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 15; i++) n[i] = lds_u32(T + 4u * nib_node(i));
+    sat = lds_u32(T + 4u) == kZeroSat && lds_u32(T + 8u) == kZeroSat && lds_u32(T + 16u) == kZeroSat &&
+          lds_u32(T + 32u) == kZeroSat;
+    return ctx & 0xFFu;
+}
+
+template <bool PREV>
+__device__ __forceinline__ void lane8_plane(uint32_t (&n)[15], bool& sat, uint32_t T, const PlaneRef& pr,
+                                            const uint32_t* __restrict__ prev, uint32_t* __restrict__ out,
+                                            uint32_t hw, uint32_t w) {
+    LaneStream ls;
+    ls.init(pr.coded, pr.coded_len);
+    uint32_t code = (uint32_t)(ls.bb >> 32);
+    ls.consume(4);
+    ls.append();
+    uint32_t rng = 0xFFFFFFFFu;
+    uint32_t left = 0, above = 0, x = 0;
+    auto sample = [&](uint32_t idx, uint32_t pw, uint32_t j) -> uint32_t {
+            const uint32_t bhi = (uint32_t)(ls.bb >> 32);
+            uint32_t a = rng >> 12, r = rng, c = code, sel = 0x2107u, rmin = 0xFFFFFFFFu, bad = 0;
+#pragma unroll
+            for (int d = 0; d < 4; d++) zstep(a, r, c, sel, rmin, bad, bhi);
+            uint32_t pn4, pn5, pn6, pn7;
+            const uint32_t b4 = fstep(a, r, c, sel, rmin, pn4, n[0], bhi);
+            const uint32_t x0 = b4 ? n[5] : n[3], x1 = b4 ? n[6] : n[4];
+            const uint32_t y00 = b4 ? n[11] : n[7], y01 = b4 ? n[12] : n[8];
+            const uint32_t y10 = b4 ? n[13] : n[9], y11 = b4 ? n[14] : n[10];
+            const uint32_t b5 = fstep(a, r, c, sel, rmin, pn5, b4 ? n[2] : n[1], bhi);
+            const uint32_t y0 = b5 ? y10 : y00, y1 = b5 ? y11 : y01;
+            const uint32_t b6 = fstep(a, r, c, sel, rmin, pn6, b5 ? x1 : x0, bhi);
+            const uint32_t b7 = fstep(a, r, c, sel, rmin, pn7, b6 ? y1 : y0, bhi);
+            const uint32_t used = 0x2107u - sel;
+            uint32_t z;
+            if (sat && bad == 0 && rmin >= (1u << 16) && used <= 4u && 8 * (int32_t)used <= ls.nbits) {
+                n[0] = pn4;
+                n[1] = b4 ? n[1] : pn5;
+                n[2] = b4 ? pn5 : n[2];
+                const uint32_t i6 = 2u * b4 + b5;
+#pragma unroll
+                for (int q = 0; q < 4; q++) n[3 + q] = i6 == (uint32_t)q ? pn6 : n[3 + q];
+                const uint32_t i7 = 4u * b4 + 2u * b5 + b6;
+#pragma unroll
+                for (int q = 0; q < 8; q++) n[7 + q] = i7 == (uint32_t)q ? pn7 : n[7 + q];
+                rng = r;
+                code = c;
+                ls.consume(used);
+                ls.append();
+                z = (b4 << 3) | (b5 << 2) | (b6 << 1) | b7;
+            } else {
+                z = lane8_careful(n, T, rng, code, ls, sat);
+            }
+            const uint32_t rr = (z >> 1) ^ (0u - (z & 1u));
+            uint32_t v;
+            if (PREV) {
+                v = ((pw >> (8 * j)) + rr) & 0xFFu;
+            } else {
+                const uint32_t pred = x > 0 ? left : (idx > 0 ? above : 0x80u);
+                v = (pred + rr) & 0xFFu;
+                above = x == 0 ? v : above;
+                left = v;
+                x = x + 1 == w ? 0u : x + 1;
+            }
+            return v << (8 * j);
+    };
+    const uint32_t full = hw / 4;
+    for (uint32_t wi = 0; wi < full; wi++) {  // 4 samples per word, unrolled
+        const uint32_t pw = PREV ? __ldg(prev + wi) : 0u;
+        uint32_t ow = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) ow |= sample(4 * wi + j, pw, j);
+        out[wi] = ow;
+    }
+    if (hw & 3u) {
+        const uint32_t pw = PREV ? __ldg(prev + full) : 0u;
+        uint32_t ow = 0;
+        for (uint32_t j = 0; j < (hw & 3u); j++) ow |= sample(4 * full + j, pw, j);
+        out[full] = ow;
+    }
+}
+
+__device__ __forceinline__ void lane8_run(const RunDesc& r, const PlaneRef* __restrict__ planes, uint32_t T) {
+    for (uint32_t i = 0; i < 256; i++) sts_u32(T + 4u * i, (i != 0 && (i & (i - 1)) == 0) ? 3686u : 2048u);
+    uint32_t n[15];
+#pragma unroll
+    for (int i = 0; i < 15; i++) n[i] = lds_u32(T + 4u * nib_node(i));
+    bool sat = false;
+    const uint32_t hw = (uint32_t)r.w * r.h;
+    for (int f = 0; f < r.count; f++) {
+        const PlaneRef pr = planes[r.plane_base + f];
+        if (pr.mode != 0) continue;
+        uint32_t* out = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(pr.samples));
+        if (f > 0)
+            lane8_plane<true>(n, sat, T, pr, reinterpret_cast<const uint32_t*>(planes[r.plane_base + f - 1].samples),
+                              out, hw, r.w);
+        else
+            lane8_plane<false>(n, sat, T, pr, nullptr, out, hw, r.w);
+    }
+}
+
 constexpr uint32_t kSpecSmem = 2 * (kRingBytes + kTreeBytes);  // per block (2 u8 runs, or 1 u16 run with 2 trees)
 
 // One launch for every width class (no serialisation of the u8 and u16 runs
@@ -1225,6 +1560,8 @@ struct RcClasses {
     int n[3];    // runs per class (1, 2, 4 bytes per sample)
     int off[3];  // first index into rc_runs
     int blk[4];  // block prefix
+    int u8_spec; // variant 5: 8-bit runs by half-warp speculation (else a lane per run)
+    int skip;    // dev isolation probe: bit k skips class k (results wrong by design)
 };
 
 template <int V>
@@ -1233,7 +1570,8 @@ __global__ void __launch_bounds__(32) rc_decode_kernel(const RunDesc* __restrict
                                                          const PlaneRef* __restrict__ planes) {
     extern __shared__ uint4 probs_s[];
     const int b = blockIdx.x;
-    if (V == 5 && b < c.blk[2]) {
+    if (V >= 5 && (c.skip >> (b < c.blk[1] ? 0 : (b < c.blk[2] ? 1 : 2)) & 1)) return;
+    if (V >= 5 && b < c.blk[2] && (c.u8_spec == 1 || b >= c.blk[1])) {
         // variant 5: blocks [0, blk1): two 8-bit runs each; [blk1, blk2): one 16-bit run each
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
         const uint32_t lane = threadIdx.x;
@@ -1249,8 +1587,8 @@ __global__ void __launch_bounds__(32) rc_decode_kernel(const RunDesc* __restrict
             if (h != 0) return;
         } else {
             gi = b - c.blk[1];
-            spec16_run(runs[rc_runs[c.off[1] + gi]], planes, base + kRingBytes, base + kRingBytes + kTreeBytes, base,
-                       lane);
+            spec16_run<V == 5>(runs[rc_runs[c.off[1] + gi]], planes, base + kRingBytes, base + kRingBytes + kTreeBytes,
+                               lane);
             gi += c.off[1];
             if (lane != 0) return;
         }
@@ -1261,11 +1599,21 @@ __global__ void __launch_bounds__(32) rc_decode_kernel(const RunDesc* __restrict
         return;
     }
     const int nb = b < c.blk[1] ? 1 : (b < c.blk[2] ? 2 : 4);
-    if constexpr (V == 5) {  // 32-bit runs: the lane-per-run decoder (variant 4)
+    if constexpr (V >= 5) {  // 32-bit (and lane-per-run 8-bit) runs: variant 4
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
         const uint32_t R = base + threadIdx.x * kRingBytes;
-        const uint32_t P = base + blockDim.x * kRingBytes + threadIdx.x * lane_stride(4);
-        decode_runs<4, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R, c.off[2]);
+        const uint32_t P = base + blockDim.x * kRingBytes + threadIdx.x * lane_stride(nb);
+        if (b < c.blk[1] && c.u8_spec == 2) {
+            const int gi = b * 32 + (int)threadIdx.x;
+            if (gi >= c.n[0]) return;
+            const long long t0 = clock64();
+            lane8_run(runs[rc_runs[c.off[0] + gi]], planes, base + threadIdx.x * (kTreeBytes + 16u));
+            if (unsigned long long* prof = g_rc_prof) {
+                prof[2 * (c.off[0] + gi)] = rc_runs[c.off[0] + gi];
+                prof[2 * (c.off[0] + gi) + 1] = (unsigned long long)(clock64() - t0);
+            }
+        } else if (b < c.blk[1]) decode_runs<4, 1>(runs, rc_runs + c.off[0], c.n[0], b, planes, P, R, c.off[0]);
+        else decode_runs<4, 4>(runs, rc_runs + c.off[2], c.n[2], b - c.blk[2], planes, P, R, c.off[2]);
     } else {
     // lane rings of coded bytes first, then the lane-private probability trees
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(probs_s);
@@ -1286,24 +1634,34 @@ void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n
     int rpw = er ? atoi(er) : kRPW;
     rpw = rpw < 1 ? 1 : (rpw > 32 ? 32 : rpw);
     const char* ev = getenv("GSV_RC_VARIANT");  // decoder variant (dev tuning)
-    const int v = ev ? atoi(ev) : 5;
+    const int v = ev ? atoi(ev) : 6;
+    const char* e8 = getenv("GSV_RC_U8_SPEC");
+    c.u8_spec = e8 ? atoi(e8) : 2;
+    const char* es = getenv("GSV_RC_SKIP");
+    c.skip = es ? atoi(es) : 0;
     c.blk[0] = 0;
     for (int k = 0; k < 3; k++) {
         c.n[k] = n_per_class[k];
         c.off[k] = off;
         off += c.n[k];
         // variant 5: 2 runs per block (8-bit), 1 (16-bit); 32-bit runs rpw per block
-        const int per = v == 5 ? (k == 0 ? 2 : (k == 1 ? 1 : 32)) : rpw;
+        const int per = v >= 5 ? (k == 0 ? (c.u8_spec == 1 ? 2 : 32) : (k == 1 ? 1 : 32)) : rpw;
         c.blk[k + 1] = c.blk[k] + (c.n[k] + per - 1) / per;
         if (c.n[k] > 0) nbmax = 1 << k;
     }
     if (c.blk[3] == 0) return;
     size_t smem = (size_t)(lane_stride(nbmax) + kRingBytes) * rpw;
-    if (v == 5) {
+    if (v >= 5) {
         smem = kSpecSmem;
+        if (c.n[0] > 0 && c.u8_spec != 1) smem = std::max(smem, (size_t)(lane_stride(1) + kRingBytes) * 32);
         if (c.n[2] > 0) smem = std::max(smem, (size_t)(lane_stride(4) + kRingBytes) * 32);
-        cudaFuncSetAttribute(rc_decode_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rc_decode_kernel<5><<<c.blk[3], 32, smem, s>>>(runs, rc_runs, c, planes);
+        if (v == 6) {
+            cudaFuncSetAttribute(rc_decode_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rc_decode_kernel<6><<<c.blk[3], 32, smem, s>>>(runs, rc_runs, c, planes);
+        } else {
+            cudaFuncSetAttribute(rc_decode_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rc_decode_kernel<5><<<c.blk[3], 32, smem, s>>>(runs, rc_runs, c, planes);
+        }
     } else if (v == 4) {
         cudaFuncSetAttribute(rc_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         rc_decode_kernel<4><<<c.blk[3], rpw, smem, s>>>(runs, rc_runs, c, planes);

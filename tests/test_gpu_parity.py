@@ -398,7 +398,7 @@ def test_truncated_coded_block_is_codec_error(gsvb, bits):
     assert gsvb.decode_planes(good)[0].samples.ravel().tolist() == d["expected_samples"][0]
 
 
-@pytest.mark.parametrize("variant", ["1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("variant", ["1", "2", "3", "4", "5", "6"])
 def test_range_decoder_variants_bit_exact(gsvb, variant, monkeypatch):
     """Every range-decoder variant (GSV_RC_VARIANT: 1 C++ fast path, 2 PTX
     step, 3 + zero-prefix test, 4 + saturated zero-prefix test, 5 warp-

@@ -36,6 +36,7 @@ for gd in info.groups:
             chan_of.append((e.channel.attribute, e.channel.component, gd.frame_count))
 L = _lib.load()
 L.gsv_dev_rc_profile.argtypes = [ctypes.c_void_p]
+L.gsv_dev_rc_slow_bytes.restype = ctypes.c_ulonglong
 prof = torch.zeros(2 * len(chan_of), dtype=torch.int64, device="cuda")
 sess = g.Session()
 base_env = dict(os.environ)
@@ -47,13 +48,20 @@ for st in settings:
         k, v = kv.split("=")
         os.environ[k] = v
     times = []
+    L.gsv_dev_rc_slow_bytes(1)
     for rep in range(2):
         prof.zero_()
         L.gsv_dev_rc_profile(ctypes.c_void_p(prof.data_ptr()))
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(sess.stream)
-        vid = g.DeviceVideo(data, 6, session=sess, resident=res, info=info)
+        try:
+            vid = g.DeviceVideo(data, 6, session=sess, resident=res, info=info)
+        except g.CodecError:  # GSV_RC_SKIP probes leave runs undecoded (by design)
+            torch.cuda.synchronize()
+            times.append(float("nan"))
+            same = None
+            continue
         e1.record(sess.stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -71,7 +79,9 @@ for st in settings:
             a, c, fc = chan_of[rid]
             per[(a, c)].append(cyc)
     hw = 224 * 224
-    print(f"== [{st or 'default'}] open {min(times):.1f} ms  codes == first setting: {same}")
+    slow = L.gsv_dev_rc_slow_bytes(1)
+    print(f"== [{st or 'default'}] open {min(times):.1f} ms  codes == first setting: {same}  "
+          f"careful-path bytes (lane calls, 2 opens) {slow}")
     rows = sorted(per.items(), key=lambda kv: -max(kv[1]))
     for (a, c), cyc in rows[:8]:
         print(f"   {a}[{c}]: runs {len(cyc)}  max {max(cyc) / 1e6:.1f} Mcyc  mean {sum(cyc) / len(cyc) / 1e6:.1f} Mcyc"
