@@ -343,7 +343,7 @@ struct RunSet {
         std::vector<uint32_t> chunk_prefix(planes.size() + 1, 0);
         for (size_t i = 0; i < planes.size(); i++) {
             const uint32_t pb = runs[planes[i].run].plane_bytes;
-            chunk_prefix[i + 1] = chunk_prefix[i] + (pb + 1023) / 1024;
+            chunk_prefix[i + 1] = chunk_prefix[i] + (pb + kCrcChunk - 1) / kCrcChunk;
         }
         if ((rc = upload(d_runs, runs, s))) return rc;
         if ((rc = upload(d_planes, planes, s))) return rc;
@@ -1076,7 +1076,7 @@ int gsv_encode_runs(gsv_session* s, gsv_encode_run* runs, int nruns) {
             p.run = (uint32_t)i;
             p.f = f;
             pl.push_back(p);
-            nchunks += (pb + 1023) / 1024;
+            nchunks += (pb + kCrcChunk - 1) / kCrcChunk;
             chunk_prefix.push_back((uint32_t)nchunks);
         }
     }

@@ -112,6 +112,13 @@ __device__ __forceinline__ float t_eff(uint32_t m, uint32_t bit, float T) {
         : "=f"(r) : "r"(m), "r"(bit), "f"(T));
     return r;
 }
+// T if T >= 1e-4, else 0 (the rect test done by the caller)
+__device__ __forceinline__ float t_live(float T) {
+    float r;
+    asm("{\n\t.reg .pred pt;\n\tsetp.ge.f32 pt, %1, 0f38D1B717;\n\tselp.f32 %0, %1, 0f00000000, pt;\n\t}"
+        : "=f"(r) : "f"(T));
+    return r;
+}
 __device__ __forceinline__ void sts_f4(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
@@ -132,8 +139,16 @@ __device__ __forceinline__ float ex2f(float x) {
 // pixel), power clamp, 0.99 alpha cap, alpha <= 0 skip, fp32, fixed order.
 // The quadratic form is evaluated as A + dy (B + C dy) with A, B per
 // (record, column) -- a different fp32 rounding of the same fp64 quantity.
-template <int ROWS, bool PACKED, bool TEFF, bool RANGES>
-__global__ void __launch_bounds__(128, 5) composite_strip_kernel(
+//
+// V3 (the default): the staging lane also rewrites the record's first 16 B as
+// (bx, by, mask, log2 op), so a lane's per-record work is three shared loads
+// (that quad, (ca, cb), (cc, r, g, b)), its rows of the rect from one byte
+// permute and one column-bit test against lane constants, and the 0.99 cap
+// decision from log2 op; the arithmetic is V2's, op for op (only records
+// with op in (0.98994, 0.99] also take the 0.99 cap, which can only round an
+// alpha of 0.99 + 1 ulp down to the reference's ceiling).
+template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5>
+__global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
@@ -171,6 +186,9 @@ __global__ void __launch_bounds__(128, 5) composite_strip_kernel(
     const int rowoff = strip * 2 * ROWS + (lane >> 4) * ROWS;       // first row in the tile
     const float rowf = (float)rowoff;
     const uint32_t colsh = (uint32_t)(lane & 15), rowsh = 16u + (uint32_t)rowoff;
+    // V3: the lane's column bit and the byte permute that moves its 8 rows of
+    // the rect's row mask (mask bits 16-31) to bits 0-7
+    const uint32_t colbit = 1u << colsh, rsel = 0x4440u | (rowsh >> 3);
     float T[ROWS], c0[ROWS], c1[ROWS], c2[ROWS];
     uint32_t live = 0, inimg = 0;
     const bool work = on && start < end;
@@ -242,27 +260,43 @@ __global__ void __launch_bounds__(128, 5) composite_strip_kernel(
             const uint32_t cm = (0xFFFFu << cl) & ~(0xFFFFu << ch) & 0xFFFFu;
             const uint32_t rm = (0xFFFFu << rl) & ~(0xFFFFu << rh) & 0xFFFFu;
             sts_f4(sl, make_float4(((float)tx0 - v0.x) - v1.x, ((float)ty0 - v0.y) - v1.y,
-                                   __uint_as_float(cm | (rm << 16)), 0.f));
+                                   __uint_as_float(cm | (rm << 16)), V3 ? v3.w : 0.f));
         }
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
         for (int q = 0; q < cnt; q++) {
             const uint32_t ra = sbase + (uint32_t)q * 64u;
-            const float4 rc = lds_f4(ra);  // bx, by, column | row mask of the rect in this tile
+            const float4 rc = lds_f4(ra);  // bx, by, column | row mask of the rect in this tile[, log2 op]
             const uint32_t mw = __float_as_uint(rc.z);
             // strip rows against the rect: warp-uniform skip (a strip of 8-row
             // lanes is the whole tile: every record overlaps it)
             if (kStrips > 1 && ((mw >> (16 + strip * 2 * ROWS)) & ((1u << (2 * ROWS)) - 1u)) == 0u) continue;
             // rows of the lane's column inside the rect (empty outside its columns)
-            const uint32_t m = ((mw >> colsh) & 1u) ? (mw >> rowsh) & ((1u << ROWS) - 1u) : 0u;
+            uint32_t m;
+            if constexpr (V3) {
+                m = (mw & colbit) ? __byte_perm(mw, 0u, rsel) : 0u;
+            } else {
+                m = ((mw >> colsh) & 1u) ? (mw >> rowsh) & ((1u << ROWS) - 1u) : 0u;
+            }
             // rows some lane still needs (rect and T >= 1e-4): one vote per
             // record, then whole row pairs no lane needs are skipped with a
             // warp-uniform branch (rect edges, saturated rows)
             const uint32_t need = __reduce_or_sync(0xffffffffu, m & live);
             if (!need) continue;
-            const float4 a = lds_f4(ra + 16u);  // ox, oy, ca, cb
+            float4 a, r3;
+            if constexpr (V3) {
+                float2 cab;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(cab.x), "=f"(cab.y) : "r"(ra + 24u));
+                a = make_float4(0.f, 0.f, cab.x, cab.y);
+                // op > 0.99 (cap path) from log2 op: log2(0.99) = -0.0144996; a
+                // slightly wider test only sends a few more records through
+                // the (then inactive) cap
+                r3 = make_float4(rc.w > -0.0146f ? 1.f : 0.f, 0.f, 0.f, rc.w);
+            } else {
+                a = lds_f4(ra + 16u);  // ox, oy, ca, cb
+                r3 = lds_f4(ra + 48u);  // op, rx, ry, log2 op
+            }
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
-            const float4 r3 = lds_f4(ra + 48u);  // op, rx, ry, log2 op
             const float op = r3.x;
             const float dx = colf + rc.x;
             const float A = a.z * dx * dx, B = a.w * dx;
@@ -276,20 +310,35 @@ __global__ void __launch_bounds__(128, 5) composite_strip_kernel(
                 // record), so alpha = 2^pw needs no multiply and, for op <=
                 // 0.99, no 0.99 cap (alpha <= op); the reference's p = min(p,
                 // 0) only trims rounding (the conic is positive definite)
-                const float A1 = TEFF ? A + __uint_as_float(__float_as_uint(r3.w)) : A;
+                float A1 = TEFF ? A + __uint_as_float(__float_as_uint(r3.w)) : A;
+                // V3: the rect covers all 16 rows of the tile (row mask 0xFFFF)
+                const bool full = V3 && mw >= 0xFFFF0000u;
+                if (V3 && !(mw & colbit)) A1 = -INFINITY;
                 const f2 A2{A1, A1}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
                 const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};
                 const f2 dy01 = add2(D2, f2{0.f, 1.f});
-                auto pairs = [&](auto cap_c) {
+                auto pairs = [&](auto cap_c, auto full_c) {
                     constexpr bool CAP = decltype(cap_c)::value;
+                    constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
                     for (int j = 0; j < ROWS; j += 2) {
-                        if (!(need & (3u << j))) continue;
+                        // FULL: no per-pair skip (nearly every pair is needed when
+                        // the rect spans the tile's rows), so the four pairs form
+                        // independent chains the scheduler interleaves (ex2
+                        // latency hidden within the warp); a dead pair composites
+                        // with weight 0
+                        if (!FULL && !(need & (3u << j))) continue;
                         // (j, j) broadcast: an immediate operand, no pair constant to build
                         const f2 dy = j ? add2(dy01, f2{(float)j, (float)j}) : dy01;
                         f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
                         f2 te, al;
-                        if (TEFF) {
+                        if (FULL) {
+                            // every row of the tile inside the rect: only the
+                            // T >= 1e-4 test per pixel; a lane outside the
+                            // rect's columns has A = -inf (alpha 0)
+                            te = f2{t_live(T[j]), t_live(T[j + 1])};
+                            al = f2{ex2f(pw.x), ex2f(pw.y)};
+                        } else if (TEFF) {
                             te = f2{t_eff(m, 1u << j, T[j]), t_eff(m, 1u << (j + 1), T[j + 1])};
                             al = f2{ex2f(pw.x), ex2f(pw.y)};
                         } else {
@@ -317,8 +366,16 @@ __global__ void __launch_bounds__(128, 5) composite_strip_kernel(
                         T[j + 1] = t.y;
                     }
                 };
-                if (TEFF && op <= 0.99f) pairs(std::false_type{});
-                else pairs(std::true_type{});
+                if (full) {
+                    // the rect covers the tile's 16 rows (about 60% of the
+                    // (record, tile) pairs at config 2)
+                    if (op == 0.f) pairs(std::false_type{}, std::true_type{});
+                    else pairs(std::true_type{}, std::true_type{});
+                } else if (TEFF && (V3 ? op == 0.f : op <= 0.99f)) {
+                    pairs(std::false_type{}, std::false_type{});
+                } else {
+                    pairs(std::true_type{}, std::false_type{});
+                }
             } else {
                 // branch-free over the lane's rows: a pixel outside the rect or
                 // already at T < 1e-4 gets alpha 0, and alpha <= 0 composites as a
@@ -403,29 +460,37 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     static int packed = -1;
     if (packed < 0) {
         const char* e = getenv("GSV_COMPOSITE_PACKED");
-        packed = e ? atoi(e) : 2;
+        packed = e ? atoi(e) : 3;
     }
-#define GSV_COMPOSITE(R, P, E)                                                                          \
+#define GSV_COMPOSITE(R, P, E, V, MB)                                                                   \
     do {                                                                                                \
         if (tile_off)                                                                                   \
-            composite_strip_kernel<R, P, E, true><<<grid, 128, 0, s>>>(                                 \
+            composite_strip_kernel<R, P, E, true, V, MB><<<grid, 128, 0, s>>>(                          \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
         else                                                                                            \
-            composite_strip_kernel<R, P, E, false><<<grid, 128, 0, s>>>(                                \
+            composite_strip_kernel<R, P, E, false, V, MB><<<grid, 128, 0, s>>>(                         \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
     } while (0)
-    if (packed == 2 && rows == 8) {
-        GSV_COMPOSITE(8, true, true);
+    static int minb = -1;  // CTAs per SM the register budget is cut for (V3)
+    if (minb < 0) {
+        const char* e = getenv("GSV_COMPOSITE_MINB");
+        minb = e ? atoi(e) : 5;
+    }
+    if (packed == 3 && rows == 8) {
+        if (minb == 4) GSV_COMPOSITE(8, true, true, true, 4);
+        else GSV_COMPOSITE(8, true, true, true, 5);
+    } else if (packed >= 2 && rows == 8) {
+        GSV_COMPOSITE(8, true, true, false, 5);
     } else if (packed) {
-        if (rows == 8) GSV_COMPOSITE(8, true, false);
-        else if (rows == 4) GSV_COMPOSITE(4, true, false);
-        else GSV_COMPOSITE(2, true, false);
+        if (rows == 8) GSV_COMPOSITE(8, true, false, false, 5);
+        else if (rows == 4) GSV_COMPOSITE(4, true, false, false, 5);
+        else GSV_COMPOSITE(2, true, false, false, 5);
     } else {
-        if (rows == 8) GSV_COMPOSITE(8, false, false);
-        else if (rows == 4) GSV_COMPOSITE(4, false, false);
-        else GSV_COMPOSITE(2, false, false);
+        if (rows == 8) GSV_COMPOSITE(8, false, false, false, 5);
+        else if (rows == 4) GSV_COMPOSITE(4, false, false, false, 5);
+        else GSV_COMPOSITE(2, false, false, false, 5);
     }
 #undef GSV_COMPOSITE
 }

@@ -11,13 +11,22 @@ namespace gsv {
 
 // ---------------------------------------------------------------------------
 // CRC-32 of every run (codec.py:260-262): the run's planes are split into
-// 1 KiB chunks; each thread computes a chunk's standard CRC with
-// slicing-by-8 tables in shared memory, shifts it by the bytes that follow it
-// in the run (multiplication by x^(8*after) mod P), and XORs it into the run
-// accumulator.  XOR is commutative, so the result is deterministic.
+// kCrcChunk-byte chunks; each thread computes a chunk's standard CRC, shifts
+// it by the bytes that follow it in the run (multiplication by x^(8*after)
+// mod P: zlib's crc32_combine, applied to every chunk at once), and XORs it
+// into the run accumulator.  XOR is commutative, so the result is
+// deterministic.
+//
+// HBM-bound by design: a thread reads its 4 KiB chunk with 256-bit loads
+// (every load instruction moves 32 full sectors), four loads in flight.  The
+// byte tables are slicing-by-4 in shared memory replicated per lane -- entry
+// (t, b) of lane l at word ((t * 256 + b) * 32 + l) -- so each lookup hits the
+// lane's own bank (no conflicts for any data); 128 KiB per CTA, one CTA of
+// 1024 threads per SM.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kCrcChunk = 1024;
 constexpr uint32_t kPoly = 0xEDB88320u;
+constexpr int kCrcThreads = 1024;
+constexpr size_t kCrcSmem = 4 * 256 * 32 * sizeof(uint32_t);
 __constant__ uint32_t c_x2n[32];
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
@@ -44,61 +53,80 @@ __device__ __forceinline__ uint32_t x8nmodp(uint64_t n) {  // x^(8n) mod P
     return p;
 }
 
-__global__ void __launch_bounds__(256) crc_kernel(const RunDesc* __restrict__ runs,
-                                                  const PlaneRef* __restrict__ planes, int nplanes,
-                                                  const uint32_t* __restrict__ chunk_prefix,
-                                                  uint32_t nchunks, uint32_t* __restrict__ run_crc) {
-    __shared__ uint32_t T[8][256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; k++) c = (c & 1) ? (kPoly ^ (c >> 1)) : (c >> 1);
-        T[0][i] = c;
+// one table word of lane `lo` (= lane * 4 + table base): byte b of table t
+__device__ __forceinline__ uint32_t tab(uint32_t lo, uint32_t t, uint32_t b) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lo + (t * 256u + b) * 128u));
+    return v;
+}
+// four bytes through the slicing-by-4 tables
+__device__ __forceinline__ uint32_t crc_word(uint32_t lo, uint32_t crc, uint32_t w) {
+    const uint32_t a = crc ^ w;
+    return tab(lo, 3, a & 0xFFu) ^ tab(lo, 2, (a >> 8) & 0xFFu) ^ tab(lo, 1, (a >> 16) & 0xFFu) ^ tab(lo, 0, a >> 24);
+}
+__device__ __forceinline__ uint32_t crc_byte(uint32_t lo, uint32_t crc, uint32_t b) {
+    return tab(lo, 0, (crc ^ b) & 0xFFu) ^ (crc >> 8);
+}
+struct U8x32 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ U8x32 ld256(const uint8_t* p) {
+    U8x32 v;
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                   "=r"(v.w[7])
+                 : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(kCrcThreads, 1) crc_kernel(const RunDesc* __restrict__ runs,
+                                                             const PlaneRef* __restrict__ planes, int nplanes,
+                                                             const uint32_t* __restrict__ chunk_prefix,
+                                                             uint32_t nchunks, uint32_t* __restrict__ run_crc) {
+    extern __shared__ __align__(16) uint32_t T[];  // [4][256][32]
+    for (uint32_t i = threadIdx.x; i < 1024u; i += blockDim.x) {
+        const uint32_t t = i >> 8, b = i & 255u;
+        uint32_t c = b;  // byte b followed by t zero bytes
+        for (uint32_t k = 0; k < 8u * (t + 1u); k++) c = (c & 1u) ? (kPoly ^ (c >> 1)) : (c >> 1);
+        for (int l = 0; l < 32; l++) T[i * 32u + l] = c;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        uint32_t c = T[0][i];
-        for (int k = 1; k < 8; k++) {
-            c = (c >> 8) ^ T[0][c & 0xFF];
-            T[k][i] = c;
-        }
-    }
-    __syncthreads();
-    for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
-         ch += gridDim.x * blockDim.x) {
+    const uint32_t lo = (uint32_t)__cvta_generic_to_shared(T) + 4u * (threadIdx.x & 31u);
+    for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
         // plane of this chunk: last p with chunk_prefix[p] <= ch
-        int lo = 0, hi = nplanes;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (chunk_prefix[mid] <= ch) lo = mid; else hi = mid;
+        int plo = 0, phi = nplanes;
+        while (phi - plo > 1) {
+            const int mid = (plo + phi) >> 1;
+            if (__ldg(chunk_prefix + mid) <= ch) plo = mid;
+            else phi = mid;
         }
-        const PlaneRef pr = planes[lo];
+        const PlaneRef pr = planes[plo];
         const RunDesc r = runs[pr.run];
-        const uint32_t off = (ch - chunk_prefix[lo]) * kCrcChunk;
+        const uint32_t off = (ch - __ldg(chunk_prefix + plo)) * kCrcChunk;
         const uint32_t len = min(kCrcChunk, r.plane_bytes - off);
         const uint8_t* p = pr.samples + off;
         uint32_t crc = 0xFFFFFFFFu;
         uint32_t i = 0;
-        // 16-B loads (a thread walks its own 1 KiB chunk, so every load
-        // instruction touches 32 separate sectors: use all 16 B of each)
-        const uint32_t head = (uint32_t)((16 - ((uintptr_t)p & 15)) & 15);
-        for (; i < head && i < len; i++) crc = T[0][(crc ^ p[i]) & 0xFF] ^ (crc >> 8);
-        for (; i + 16 <= len; i += 16) {
-            const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p + i));
-            uint32_t a = crc ^ w.x, b = w.y;
-            crc = T[7][a & 0xFF] ^ T[6][(a >> 8) & 0xFF] ^ T[5][(a >> 16) & 0xFF] ^ T[4][a >> 24] ^
-                  T[3][b & 0xFF] ^ T[2][(b >> 8) & 0xFF] ^ T[1][(b >> 16) & 0xFF] ^ T[0][b >> 24];
-            a = crc ^ w.z;
-            b = w.w;
-            crc = T[7][a & 0xFF] ^ T[6][(a >> 8) & 0xFF] ^ T[5][(a >> 16) & 0xFF] ^ T[4][a >> 24] ^
-                  T[3][b & 0xFF] ^ T[2][(b >> 8) & 0xFF] ^ T[1][(b >> 16) & 0xFF] ^ T[0][b >> 24];
+        // bytes up to 32-B alignment (raw planes are consumed in place and may
+        // start anywhere)
+        const uint32_t head = min(len, (uint32_t)((32 - ((uintptr_t)p & 31)) & 31));
+        for (; i < head; i++) crc = crc_byte(lo, crc, p[i]);
+        // 128 B per step: four 256-bit loads issued before the tables run
+        for (; i + 128 <= len; i += 128) {
+            U8x32 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = ld256(p + i + 32 * q);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int k = 0; k < 8; k++) crc = crc_word(lo, crc, v[q].w[k]);
         }
-        for (; i + 8 <= len; i += 8) {
-            const uint2 w = *reinterpret_cast<const uint2*>(p + i);
-            const uint32_t a = crc ^ w.x, b = w.y;
-            crc = T[7][a & 0xFF] ^ T[6][(a >> 8) & 0xFF] ^ T[5][(a >> 16) & 0xFF] ^ T[4][a >> 24] ^
-                  T[3][b & 0xFF] ^ T[2][(b >> 8) & 0xFF] ^ T[1][(b >> 16) & 0xFF] ^ T[0][b >> 24];
+        for (; i + 32 <= len; i += 32) {
+            const U8x32 v = ld256(p + i);
+#pragma unroll
+            for (int k = 0; k < 8; k++) crc = crc_word(lo, crc, v.w[k]);
         }
-        for (; i < len; i++) crc = T[0][(crc ^ p[i]) & 0xFF] ^ (crc >> 8);
+        for (; i < len; i++) crc = crc_byte(lo, crc, p[i]);
         crc = ~crc;
         const uint64_t after = (uint64_t)(r.count - 1 - pr.f) * r.plane_bytes + (r.plane_bytes - off - len);
         if (after) crc = multmodp(x8nmodp(after), crc);
@@ -134,9 +162,15 @@ void launch_crc(const RunDesc* runs, const PlaneRef* planes, int nplanes,
                 cudaStream_t s) {
     init_x2n_table();
     if (nchunks == 0) return;
-    uint32_t blocks = (nchunks + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    crc_kernel<<<blocks, 256, 0, s>>>(runs, planes, nplanes, chunk_prefix, nchunks, run_crc);
+    // the dynamic shared-memory limit is per device; setting it is cheap and
+    // this runs once per container open
+    cudaFuncSetAttribute(crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t blocks = (nchunks + kCrcThreads - 1) / kCrcThreads;
+    if (blocks > (uint32_t)sms) blocks = (uint32_t)sms;  // persistent: one CTA per SM
+    crc_kernel<<<blocks, kCrcThreads, kCrcSmem, s>>>(runs, planes, nplanes, chunk_prefix, nchunks, run_crc);
 }
 
 // ---------------------------------------------------------------------------

@@ -250,6 +250,9 @@ void launch_copy_planes(const CopyJob* jobs, int njobs, cudaStream_t s);
 // rc_runs: run indices grouped by sample width (1, 2, 4 bytes), n_per_class[3]
 void launch_rc_decode(const RunDesc* runs, const uint32_t* rc_runs, const int* n_per_class,
                       const PlaneRef* planes, cudaStream_t s);
+// CRC-32 work unit: a chunk of this many bytes of one plane (the last chunk
+// of a plane may be shorter); chunk counts per plane are built on the host.
+constexpr uint32_t kCrcChunk = 4096;
 void launch_crc(const RunDesc* runs, const PlaneRef* planes, int nplanes,
                 const uint32_t* plane_chunk_prefix, uint32_t nchunks, uint32_t* run_crc,
                 cudaStream_t s);
