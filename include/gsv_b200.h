@@ -170,6 +170,19 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
                            uint8_t* const* host_rgb8, int nstreams, int check);
 /* after unchecked batches: GSV_OK, or GSV_E_NOMEM if any frame overflowed */
 int gsv_session_check_capacity(gsv_session* s);
+/* Decode + render every frame of the listed groups (all groups when groups
+ * is NULL) straight from host container bytes into host u8 RGB frames
+ * (host_rgb8[j]: frame j in group-list order, group-major; pinned memory
+ * makes the copies asynchronous): the reference's decode_video(path, k)
+ * followed by render_set + write_ppm's rounding of every frame
+ * (pipeline.py:350-359, render.py:382-385, 165-169; cli.py:122-131 per
+ * frame), pipelined in one call -- group uploads, opens and renders with
+ * read-back overlap; CRC and structural errors are reported as decode_video
+ * raises them (first in decode order), after the pipeline has drained.
+ * frames_out (may be NULL): frames written. */
+int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer,
+                             const int32_t* groups, int ngroups, const gsv_camera* cam,
+                             uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out);
 /* render an fp64 SoA Gaussian set resident in HBM (render_set) */
 int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos,
                    const double* rot, const double* scl, const double* opac, const double* sh,

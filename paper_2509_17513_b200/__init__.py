@@ -15,7 +15,7 @@ __version__ = "0.1.0"
 _API = ("DeviceVideo", "Session", "analyze_rd", "d_ssim", "decode_planes", "decode_video",
         "default_session", "load_raw_floats", "project_debug", "psnr", "read_container_info", "read_layers",
         "read_structure", "reconstruct_frame", "reconstruct_frame_tensors", "render",
-        "render_progressive", "render_set", "render_soa_tensors", "ssim", "write_ppm",
+        "render_progressive", "render_sequence", "render_set", "render_soa_tensors", "ssim", "write_ppm",
         "write_raw_floats")
 
 

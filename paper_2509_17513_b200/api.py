@@ -475,6 +475,64 @@ def decode_video(source, up_to_layer: int | None = None) -> DecodedVideo:
     return read_layers(source, up_to_layer)
 
 
+def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, out: torch.Tensor | None = None,
+                    streams: int = 8, session: Session | None = None, info: ContainerInfo | None = None
+                    ) -> torch.Tensor:
+    """Every frame of a container (or of the listed groups), decoded at
+    prefix k and rendered, as u8 RGB in host memory: the reference's
+    `decode_video(path, k)` followed by `render_set(video.frame(t), cam)` and
+    write_ppm's rounding for every t (pipeline.py:350-359, render.py:382-385,
+    165-169), in one pipelined call (gsv_render_sequence_host): group uploads,
+    opens and frame renders with their read-back overlap, and the reference's
+    exceptions are raised after the pipeline drains.
+
+    source: container bytes or a host uint8 tensor (pinned memory makes the
+    uploads asynchronous); out: optional host uint8 tensor (frames, H, W, 3),
+    pinned for asynchronous read-back.  Returns `out` (frames in group-list
+    order, group-major)."""
+    s = session or default_session()
+    if isinstance(source, torch.Tensor):
+        if source.is_cuda or source.dtype != torch.uint8:
+            raise InvalidInputError("source tensor must be a host uint8 tensor")
+        src = source.contiguous()
+        hptr, nbytes = src.data_ptr(), src.numel()
+        want = 1 << 16
+        while info is None:  # header + directory: grow the read until the parser is satisfied
+            try:
+                info = _structure_from_bytes(bytes(src[:min(nbytes, want)].numpy()))
+            except FormatError as e:
+                if "unexpected end" in str(e) and want < nbytes:
+                    want *= 4
+                    continue
+                raise
+    else:
+        src = _read_all(source)
+        hptr, nbytes = src, len(src)
+        if info is None:
+            info = _structure_from_bytes(src)
+    gl = list(range(len(info.groups))) if groups is None else [int(g) for g in groups]
+    for g in gl:
+        if not 0 <= g < len(info.groups):
+            raise InvalidInputError(f"group {g} out of range 0..{len(info.groups) - 1}")
+    nfr = sum(int(info.groups[g].frame_count) for g in gl)
+    c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
+    H, W = int(c.height), int(c.width)
+    if out is None:
+        out = torch.empty((nfr, H, W, 3), dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+    if out.shape != (nfr, H, W, 3) or out.dtype != torch.uint8 or out.is_cuda or not out.is_contiguous():
+        raise InvalidInputError(f"out must be a contiguous host uint8 tensor of shape {(nfr, H, W, 3)}")
+    base, step = out.data_ptr(), H * W * 3
+    ptrs = (ctypes.c_void_p * max(1, nfr))(*[base + j * step for j in range(nfr)])
+    arr = (ctypes.c_int32 * max(1, len(gl)))(*gl)
+    k = -1 if up_to_layer is None else int(up_to_layer)
+    written = ctypes.c_int64(0)
+    _pre(s)
+    check(s.lib.gsv_render_sequence_host(s.handle, hptr, nbytes, k, arr, len(gl), ctypes.byref(c), ptrs,
+                                         int(streams), ctypes.byref(written)))
+    _post(s)
+    return out
+
+
 def decode_planes(payload) -> list:
     """decode_planes (codec.py:226-263) on the GPU: list of Plane."""
     blob = payload.to_bytes() if hasattr(payload, "to_bytes") else bytes(payload)

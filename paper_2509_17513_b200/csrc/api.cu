@@ -45,6 +45,11 @@ struct gsv_session {
     cudaEvent_t ev_fork = nullptr;
     std::vector<cudaEvent_t> ev_join;
     int64_t kcap_hint = 0;
+    // gsv_render_sequence_host: group uploads on their own stream into a ring
+    // of device slots; per slot an "uploaded" event and per (slot, aux
+    // stream) a "rendered" event
+    cudaStream_t copy_in = nullptr;
+    std::vector<cudaEvent_t> ev_up, ev_slot_done;
 };
 
 namespace {
@@ -303,8 +308,21 @@ struct RunSet {
         runs.push_back(r);
     }
 
-    // allocate RC outputs, upload descriptors, decode, CRC, read CRCs back.
-    int decode(cudaStream_t s) {
+    uint32_t* hcrc = nullptr;      // pinned read-back of the CRCs (deferred mode)
+
+    // launch() state kept between prepare() and launch()
+    std::vector<CopyJob> jobs;
+    int n_cls[3] = {0, 0, 0};
+    uint32_t nchunks = 0;
+
+    // allocate RC outputs, upload descriptors, decode, CRC, read CRCs back
+    // (deferred: the read-back is only enqueued; fetch_crc() after a sync).
+    int decode(cudaStream_t s, bool deferred = false) {
+        if (int rc = prepare(s)) return rc;
+        return launch(s, deferred);
+    }
+    // descriptors and output storage: host work + small uploads only
+    int prepare(cudaStream_t s) {
         // every plane of a range-coded run gets 16-B aligned storage: RC planes
         // are decoded there, RAW planes are copied there (aligned predictors)
         size_t buf = 0;
@@ -317,7 +335,7 @@ struct RunSet {
         }
         int rc = d_planebuf.alloc(buf + 64);
         if (rc) return rc;
-        std::vector<CopyJob> jobs;
+        jobs.clear();
         for (size_t i = 0; i < planes.size(); i++) {
             if (runs[planes[i].run].kind != 1) continue;
             uint8_t* dst = d_planebuf.as<uint8_t>() + off[i];
@@ -351,26 +369,39 @@ struct RunSet {
         if ((rc = upload(d_chunk, chunk_prefix, s))) return rc;
         if ((rc = d_crc.alloc(std::max<size_t>(runs.size(), 1) * 4))) return rc;
         GSV_CUDA(cudaMemsetAsync(d_crc.p, 0, std::max<size_t>(runs.size(), 1) * 4, s));
+        for (int b = 0; b < 3; b++) n_cls[b] = (int)rc_runs[b].size();
+        nchunks = chunk_prefix.back();
+        return GSV_OK;
+    }
+    // the decode kernels (copy of RAW planes, range decode, CRC) and the CRC
+    // read-back; the payload bytes must be on the device by now (stream order)
+    int launch(cudaStream_t s, bool deferred) {
         prof_mark(ST_RCDEC, s);
         launch_copy_planes(d_jobs.as<CopyJob>(), (int)jobs.size(), s);
         if (!jobs.empty()) count_launch();
-        const int n_cls[3] = {(int)rc_runs[0].size(), (int)rc_runs[1].size(), (int)rc_runs[2].size()};
         launch_rc_decode(d_runs.as<RunDesc>(), d_rc.as<uint32_t>(), n_cls, d_planes.as<PlaneRef>(), s);
-        if (!rc_all.empty()) count_launch();
+        if (n_cls[0] + n_cls[1] + n_cls[2]) count_launch();
         prof_mark(ST_CRC, s);
         launch_crc(d_runs.as<RunDesc>(), d_planes.as<PlaneRef>(), (int)planes.size(),
-                   d_chunk.as<uint32_t>(), chunk_prefix.back(), d_crc.as<uint32_t>(), s);
-        if (chunk_prefix.back()) count_launch();
+                   d_chunk.as<uint32_t>(), nchunks, d_crc.as<uint32_t>(), s);
+        if (nchunks) count_launch();
         prof_mark(ST_COUNT, s);
         crc.assign(runs.size(), 0);
-        uint32_t* hcrc = runs.empty() ? nullptr : reinterpret_cast<uint32_t*>(t_stage.reserve(runs.size() * 4, s));
-        if (!runs.empty())
+        hcrc = runs.empty() ? nullptr : reinterpret_cast<uint32_t*>(t_stage.reserve(runs.size() * 4, s));
+        if (!runs.empty()) {
+            if (!hcrc && deferred) return fail(GSV_E_CUDA, "pinned staging unavailable");
             GSV_CUDA(cudaMemcpyAsync(hcrc ? (void*)hcrc : (void*)crc.data(), d_crc.p, runs.size() * 4,
                                      cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
-        if (hcrc) memcpy(crc.data(), hcrc, runs.size() * 4);
+        }
         GSV_CUDA(cudaGetLastError());
+        if (deferred) return GSV_OK;
+        GSV_CUDA(cudaStreamSynchronize(s));
+        fetch_crc();
         return GSV_OK;
+    }
+    void fetch_crc() {
+        if (hcrc) memcpy(crc.data(), hcrc, runs.size() * 4);
+        hcrc = nullptr;
     }
 };
 
@@ -387,14 +418,49 @@ struct gsv_video {
     std::vector<size_t> frame_base;  // by group-major frame number
     std::vector<std::vector<uint32_t>> layer_off;  // per group prefix sums
     int64_t frame_total = 0;
+    // deferred open (gsv_render_sequence_host): errors that need the CRCs are
+    // resolved by finish_open() after the stream has drained
+    ErrKey stop, pending;
+    std::vector<int64_t> run_order;
+    std::vector<std::string> run_name;
 };
 
 namespace {
 
+// The error decode_video would raise first (in the reference's order: entry
+// sequence, then phase), given the CRCs; GSV_OK when the container is clean.
+int finish_open(gsv_video* v) {
+    ErrKey best = v->stop;
+    if (v->pending.set() && (!best.set() || v->pending.order < best.order ||
+                             (v->pending.order == best.order && v->pending.phase < best.phase)))
+        best = v->pending;
+    for (size_t r = 0; r < v->runs.runs.size(); r++) {
+        if (v->runs.crc[r] != v->runs.runs[r].checksum) {
+            const int64_t o = v->run_order[r];
+            if (!best.set() || o < best.order || (o == best.order && 1 < best.phase))
+                best = {o, 1, GSV_E_CODEC, v->run_name[r] + "checksum mismatch (corrupt or truncated payload)"};
+            break;  // runs are in order: the first mismatch is the earliest
+        }
+    }
+    if (best.set()) return fail(best.kind, best.msg);
+    return GSV_OK;
+}
+
+// deferred: nothing synchronises -- the decode, CRC, table uploads and the
+// CRC read-back are enqueued on the session stream, the pinned staging is not
+// reset (the caller resets it once it has drained the stream), frame tables
+// are built whatever the CRCs say, and finish_open() reports the error after
+// a sync.  Structural errors found on the host still fail at once.
+// prepare_only (implies deferred): host work and descriptor uploads only;
+// open_launch() enqueues the decode kernels later, once the payload bytes have
+// been uploaded (gsv_render_sequence_host enqueues every group's descriptor
+// uploads before the big payload uploads, so they never queue behind them).
 int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
-               int up_to_layer, gsv_video** out, const std::vector<int>* sel = nullptr) {
+               int up_to_layer, gsv_video** out, const std::vector<int>* sel = nullptr, bool deferred = false,
+               bool prepare_only = false) {
+    if (prepare_only) deferred = true;
     *out = nullptr;
-    t_stage.reset();
+    if (!deferred) t_stage.reset();
     static const bool dbg_t = getenv("GSV_DEBUG_OPEN_TIMING") != nullptr;  // dev: phase times to stderr
     auto T = [&](const char* what) {
         static thread_local std::chrono::steady_clock::time_point last;
@@ -412,6 +478,11 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     };
     int rc = parse_container(data, len, &v->c);
     if (rc) return bail(rc);
+    // container index of each opened group (error messages name the group as
+    // decode_video of the whole container would)
+    std::vector<int> gidx(v->c.groups.size());
+    for (size_t g = 0; g < gidx.size(); g++) gidx[g] = (int)g;
+    if (sel) gidx = *sel;
     if (sel) {  // keep the selected groups only, in list order (only their bytes are staged)
         const int G0 = (int)v->c.groups.size();
         if (sel->empty()) return bail(fail(GSV_E_INVALID_INPUT, "empty group list"));
@@ -482,10 +553,10 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     const int shdim_ok = c.sh_degree <= 3;
     const int shdim = shdim_ok ? 3 * (c.sh_degree + 1) * (c.sh_degree + 1) : 0;
     v->nslots = 11 + shdim;
-    ErrKey stop;     // first structural / group-level error (walk stops there)
-    ErrKey pending;  // first post-CRC error (plane count, valid count)
-    std::vector<int64_t> run_order;            // entry sequence number of each run
-    std::vector<std::string> run_name;         // "group g layer l channel a[c]"
+    ErrKey& stop = v->stop;        // first structural / group-level error (walk stops there)
+    ErrKey& pending = v->pending;  // first post-CRC error (plane count, valid count)
+    std::vector<int64_t>& run_order = v->run_order;      // entry sequence number of each run
+    std::vector<std::string>& run_name = v->run_name;    // "group g layer l channel a[c]"
     struct SlotRef { int run = -1; const Entry* e = nullptr; };
     std::vector<std::vector<std::vector<SlotRef>>> slots(G);
     int64_t seq = 0;
@@ -498,7 +569,8 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
             for (const Entry& e : gd.channels[l]) {
                 const int64_t o = seq++;
                 char nm[96];
-                snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", g, l + 1, attr_name(e.attr), e.comp);
+                snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", gidx[g], l + 1, attr_name(e.attr),
+                         e.comp);
                 if (e.offset > len || e.size > len - e.offset) {
                     stop = {o, 0, GSV_E_FORMAT,
                             "unexpected end of container (wanted " + std::to_string(e.size) + " bytes)"};
@@ -550,22 +622,17 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     }
 
     T("walk");
+    // a structural error stops the walk: decode_video raises it unless an
+    // earlier entry's CRC fails, so such an open is resolved synchronously
+    if (stop.set()) deferred = prepare_only = false;
     // ---- decode + CRC on the GPU ------------------------------------------
-    if ((rc = v->runs.decode(st))) return bail(rc);
-    T("decode+crc");
-    ErrKey best = stop;
-    if (pending.set() && (!best.set() || pending.order < best.order ||
-                          (pending.order == best.order && pending.phase < best.phase)))
-        best = pending;
-    for (size_t r = 0; r < v->runs.runs.size(); r++) {
-        if (v->runs.crc[r] != v->runs.runs[r].checksum) {
-            const int64_t o = run_order[r];
-            if (!best.set() || o < best.order || (o == best.order && 1 < best.phase))
-                best = {o, 1, GSV_E_CODEC, run_name[r] + "checksum mismatch (corrupt or truncated payload)"};
-            break;  // runs are in order: the first mismatch is the earliest
-        }
+    if (prepare_only) {
+        if ((rc = v->runs.prepare(st))) return bail(rc);
+    } else if ((rc = v->runs.decode(st, deferred))) {
+        return bail(rc);
     }
-    if (best.set()) return bail(fail(best.kind, best.msg));
+    T("decode+crc");
+    if (!deferred && (rc = finish_open(v))) return bail(rc);
 
     // ---- frame tables: per frame, per layer, per slot the resolved plane ----
     std::vector<SlotDesc> sd;
@@ -598,7 +665,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     }
     T("frame tables");
     if ((rc = upload(v->d_slots, sd, st))) return bail(rc);
-    GSV_CUDA(cudaStreamSynchronize(st));
+    if (!deferred) GSV_CUDA(cudaStreamSynchronize(st));
     T("upload");
     *out = v;
     return GSV_OK;
@@ -667,6 +734,12 @@ void gsv_session_destroy(gsv_session* s) {
         cudaEventDestroy(s->ev_copy_join[i]);
     }
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->copy_in) {
+        cudaStreamSynchronize(s->copy_in);
+        cudaStreamDestroy(s->copy_in);
+    }
+    for (cudaEvent_t e : s->ev_up) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->ev_slot_done) cudaEventDestroy(e);
     work_free(&s->work);
     if (s->own_stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -775,13 +848,11 @@ int gsv_video_render(gsv_video* v, int t, const gsv_camera* cam, float* out_rgb,
     return render_planes(src, make_cam(*cam), &v->s->work, out_rgb, out_rgb8, stats, v->s->stream);
 }
 
-int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const gsv_camera* cam,
-                           float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8,
-                           int nstreams, int check) {
-    gsv_session* s = v->s;
-    if (count <= 0) return GSV_OK;
-    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
-    nstreams = std::max(1, std::min(nstreams, 32));
+namespace {
+
+// Aux streams, their workspaces, u8 staging buffers and events for
+// frame-parallel rendering (created on first use, grown on demand).
+int ensure_aux(gsv_session* s, int nstreams, size_t img8, bool host_out) {
     while ((int)s->aux.size() < nstreams) {
         cudaStream_t st;
         GSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -809,69 +880,292 @@ int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const
         }
     }
     if (!s->ev_fork) GSV_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    const int64_t khint = std::max(s->kcap_hint, s->work.cap_k);
+    for (int i = 0; i < nstreams; i++) {
+        if (s->aux_work[i]->cap_k < khint) {
+            int rc = work_reserve(s->aux_work[i], 1, khint, 0, 0);
+            if (rc) return rc;
+        }
+        for (int b = 0; b < 2 && host_out; b++) {
+            const int q = 2 * i + b;
+            if (s->aux_u8_cap[q] < img8) {
+                GSV_CUDA(cudaStreamSynchronize(s->aux_copy[i]));
+                if (s->aux_u8[q]) cudaFree(s->aux_u8[q]);
+                GSV_CUDA(cudaMalloc(&s->aux_u8[q], img8));
+                s->aux_u8_cap[q] = img8;
+            }
+        }
+    }
+    return GSV_OK;
+}
+
+// Enqueue frames[0..count) of v on the aux streams (frame j on stream
+// (first + j) % nstreams), forked from the session stream; host_rgb8 outputs
+// go through the per-stream double-buffered u8 staging and a copy stream.
+// Nothing is joined back into the session stream.
+int enqueue_frames(gsv_video* v, const int32_t* frames, int count, const CamDev& cd, size_t img8,
+                   float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8, int nstreams,
+                   int first) {
+    gsv_session* s = v->s;
+    GSV_CUDA(cudaEventRecord(s->ev_fork, s->stream));
+    for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_fork, 0));
+    for (int j = 0; j < count; j++) {
+        const int i = (first + j) % nstreams;
+        FrameSrc src;
+        int rc = frame_src(v, frames[j], &src);
+        if (rc) return rc;
+        uint8_t* o8 = out_rgb8 ? out_rgb8[j] : nullptr;
+        const bool to_host = host_rgb8 && host_rgb8[j];
+        int q = 0;
+        if (to_host) {
+            q = 2 * i + s->aux_flip[i];
+            s->aux_flip[i] ^= 1;
+            GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_copied[q], 0));  // staging buffer free
+            o8 = s->aux_u8[q];
+        }
+        rc = render_planes(src, cd, s->aux_work[i], out_rgb ? out_rgb[j] : nullptr, o8,
+                           reinterpret_cast<gsv_render_stats*>(1), s->aux[i]);
+        if (rc) return rc;
+        if (to_host) {
+            GSV_CUDA(cudaEventRecord(s->ev_rendered[q], s->aux[i]));
+            GSV_CUDA(cudaStreamWaitEvent(s->aux_copy[i], s->ev_rendered[q], 0));
+            GSV_CUDA(cudaMemcpyAsync(host_rgb8[j], o8, img8, cudaMemcpyDeviceToHost, s->aux_copy[i]));
+            GSV_CUDA(cudaEventRecord(s->ev_copied[q], s->aux_copy[i]));
+        }
+    }
+    return GSV_OK;
+}
+
+// Counters of every aux workspace read back, and the aux (and copy) streams
+// joined into the session stream.
+int join_aux(gsv_session* s, int nstreams, bool host_out) {
+    for (int i = 0; i < nstreams; i++) {
+        if (int rc = readback_counters(s->aux_work[i], s->aux[i])) return rc;
+        GSV_CUDA(cudaEventRecord(s->ev_join[i], s->aux[i]));
+        GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join[i], 0));
+        if (host_out) {
+            GSV_CUDA(cudaEventRecord(s->ev_copy_join[i], s->aux_copy[i]));
+            GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_copy_join[i], 0));
+        }
+    }
+    return GSV_OK;
+}
+
+// After a synchronised batch: the largest key count any aux workspace needed
+// beyond its capacity (0: every frame fitted).
+int64_t aux_key_overflow(gsv_session* s, int nstreams) {
+    int64_t need = 0;
+    for (int i = 0; i < nstreams; i++) {
+        RenderWork* w = s->aux_work[i];
+        if (w->h_ctr && (int64_t)w->h_ctr[9] > w->cap_k) need = std::max(need, (int64_t)w->h_ctr[9]);
+    }
+    return need;
+}
+
+}  // namespace
+
+int gsv_video_render_batch(gsv_video* v, const int32_t* frames, int count, const gsv_camera* cam,
+                           float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8,
+                           int nstreams, int check) {
+    gsv_session* s = v->s;
+    if (count <= 0) return GSV_OK;
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    nstreams = std::max(1, std::min(nstreams, 32));
     const CamDev cd = make_cam(*cam);
     const size_t img8 = (size_t)cam->width * cam->height * 3;
     for (int attempt = 0; attempt < 4; attempt++) {
-        const int64_t khint = std::max(s->kcap_hint, s->work.cap_k);
-        for (int i = 0; i < nstreams; i++) {
-            if (s->aux_work[i]->cap_k < khint) {
-                int rc = work_reserve(s->aux_work[i], 1, khint, 0, 0);
-                if (rc) return rc;
-            }
-            for (int b = 0; b < 2 && host_rgb8; b++) {
-                const int q = 2 * i + b;
-                if (s->aux_u8_cap[q] < img8) {
-                    GSV_CUDA(cudaStreamSynchronize(s->aux_copy[i]));
-                    if (s->aux_u8[q]) cudaFree(s->aux_u8[q]);
-                    GSV_CUDA(cudaMalloc(&s->aux_u8[q], img8));
-                    s->aux_u8_cap[q] = img8;
-                }
-            }
-        }
-        GSV_CUDA(cudaEventRecord(s->ev_fork, s->stream));
-        for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_fork, 0));
-        for (int j = 0; j < count; j++) {
-            const int i = j % nstreams;
-            FrameSrc src;
-            int rc = frame_src(v, frames[j], &src);
-            if (rc) return rc;
-            uint8_t* o8 = out_rgb8 ? out_rgb8[j] : nullptr;
-            const bool to_host = host_rgb8 && host_rgb8[j];
-            int q = 0;
-            if (to_host) {
-                q = 2 * i + s->aux_flip[i];
-                s->aux_flip[i] ^= 1;
-                GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_copied[q], 0));  // staging buffer free
-                o8 = s->aux_u8[q];
-            }
-            rc = render_planes(src, cd, s->aux_work[i], out_rgb ? out_rgb[j] : nullptr, o8,
-                               reinterpret_cast<gsv_render_stats*>(1), s->aux[i]);
-            if (rc) return rc;
-            if (to_host) {
-                GSV_CUDA(cudaEventRecord(s->ev_rendered[q], s->aux[i]));
-                GSV_CUDA(cudaStreamWaitEvent(s->aux_copy[i], s->ev_rendered[q], 0));
-                GSV_CUDA(cudaMemcpyAsync(host_rgb8[j], o8, img8, cudaMemcpyDeviceToHost, s->aux_copy[i]));
-                GSV_CUDA(cudaEventRecord(s->ev_copied[q], s->aux_copy[i]));
-            }
-        }
-        for (int i = 0; i < nstreams; i++) {
-            if (int rc = readback_counters(s->aux_work[i], s->aux[i])) return rc;
-            GSV_CUDA(cudaEventRecord(s->ev_join[i], s->aux[i]));
-            GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join[i], 0));
-            if (host_rgb8) {
-                GSV_CUDA(cudaEventRecord(s->ev_copy_join[i], s->aux_copy[i]));
-                GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_copy_join[i], 0));
-            }
-        }
+        if (int rc = ensure_aux(s, nstreams, img8, host_rgb8 != nullptr)) return rc;
+        if (int rc = enqueue_frames(v, frames, count, cd, img8, out_rgb, out_rgb8, host_rgb8, nstreams, 0)) return rc;
+        if (int rc = join_aux(s, nstreams, host_rgb8 != nullptr)) return rc;
         if (!check) return GSV_OK;
         GSV_CUDA(cudaStreamSynchronize(s->stream));
-        int64_t need = 0;
-        for (int i = 0; i < nstreams; i++) {
-            RenderWork* w = s->aux_work[i];
-            if (w->h_ctr && (int64_t)w->h_ctr[9] > w->cap_k) need = std::max(need, (int64_t)w->h_ctr[9]);
-        }
+        const int64_t need = aux_key_overflow(s, nstreams);
         if (need == 0) return GSV_OK;
         s->kcap_hint = need + need / 4 + 1024;  // grow and render the batch again
+    }
+    return fail(GSV_E_NOMEM, "tile key buffer could not be sized");
+}
+
+// ---------------------------------------------------------------------------
+// Decode + render a whole sequence from host bytes into host u8 frames: the
+// reference's decode_video + render_set + write_ppm of every frame
+// (pipeline.py:350-359, render.py:382-385, 165-169; cli.py:122-131 per frame)
+// as one pipelined call.  Raw groups (codec 0, or codec 1's whole-run raw
+// fallback) go through a ring of kSeqSlots device slots: group g's
+// layer-prefix bytes are uploaded on the copy stream while earlier groups
+// render, its runs are opened (CRC enqueued, not waited for) on the session
+// stream once they have landed, and its frames render on the aux streams with
+// their read-back; nothing on the host waits until the end, where every
+// group's CRC is checked and the first error in decode order is returned
+// (the frames written so far are then undefined, as decode_video would have
+// raised before rendering).  Sequences with range-coded runs are opened whole
+// (every run of every group decodes in parallel) and then rendered.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kSeqSlots = 3;
+
+struct VideoList {
+    std::vector<gsv_video*> v;
+    ~VideoList() {
+        for (gsv_video* x : v) delete x;
+    }
+};
+
+bool group_is_raw(const uint8_t* data, size_t len, const GroupDir& gd, int k) {
+    for (int l = 0; l < k; l++)
+        for (const Entry& e : gd.channels[l]) {
+            if (e.offset > len || e.size > len - e.offset || e.size < 15) return false;
+            const uint8_t* b = data + e.offset;
+            if (!(b[0] == 0 || (b[0] == 1 && b[14] == 1))) return false;
+        }
+    return true;
+}
+}  // namespace
+
+int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer,
+                             const int32_t* groups, int ngroups, const gsv_camera* cam,
+                             uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
+    GSV_CUDA(cudaSetDevice(s->device));
+    if (frames_out) *frames_out = 0;
+    if (!host_rgb8) return fail(GSV_E_INVALID_INPUT, "host_rgb8 is NULL");
+    if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
+    nstreams = std::max(1, std::min(nstreams, 32));
+    Container c;
+    if (int rc = parse_container(data, len, &c)) return rc;
+    std::vector<int> sel;
+    if (groups && ngroups > 0) sel.assign(groups, groups + ngroups);
+    else
+        for (int g = 0; g < (int)c.groups.size(); g++) sel.push_back(g);
+    for (int g : sel)
+        if (g < 0 || g >= (int)c.groups.size())
+            return fail(GSV_E_INVALID_INPUT, "group " + std::to_string(g) + " out of range 0.." +
+                                                 std::to_string((int)c.groups.size() - 1));
+    const int L = c.layer_count;
+    const int k = up_to_layer == -1 ? L : up_to_layer;
+    if (k < 1 || k > L)
+        return fail(GSV_E_INVALID_INPUT,
+                    "layer " + std::to_string(up_to_layer) + " out of range 1.." + std::to_string(L));
+    const CamDev cd = make_cam(*cam);
+    const size_t img8 = (size_t)cam->width * cam->height * 3;
+    bool raw = true;
+    for (int g : sel) raw = raw && group_is_raw(data, len, c.groups[g], k);
+
+    if (!raw || sel.size() < 2) {
+        gsv_video* v = nullptr;
+        if (int rc = open_video(s, data, len, nullptr, k, &v, &sel)) return rc;
+        std::vector<int32_t> fr((size_t)v->frame_total);
+        for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
+        int rc = gsv_video_render_batch(v, fr.data(), (int)fr.size(), cam, nullptr, nullptr, host_rgb8, nstreams, 1);
+        cudaStreamSynchronize(s->stream);
+        if (!rc && frames_out) *frames_out = v->frame_total;
+        delete v;
+        return rc;
+    }
+
+    // ---- raw groups: the upload / open / render pipeline -------------------
+    const int G = (int)sel.size();
+    std::vector<uint64_t> lo(G, 0), hi(G, 0);
+    uint64_t slot_bytes = 0;
+    for (int gi = 0; gi < G; gi++) {
+        bool any = false;
+        for (int l = 0; l < k; l++)
+            for (const Entry& e : c.groups[sel[gi]].channels[l]) {
+                const uint64_t end = e.offset + e.size;  // in range: group_is_raw checked it
+                lo[gi] = any ? std::min(lo[gi], e.offset) : e.offset;
+                hi[gi] = any ? std::max(hi[gi], end) : end;
+                any = true;
+            }
+        slot_bytes = std::max(slot_bytes, hi[gi] - lo[gi]);
+    }
+    // Every group gets its own slot when the prefix bytes fit comfortably in
+    // HBM (a quarter of the free memory): then all uploads are enqueued before
+    // any render, so the copy engine streams the container at PCIe rate no
+    // matter how far the host's render enqueue runs ahead.  Otherwise a ring
+    // of kSeqSlots slots, each reused once its group has rendered.
+    uint64_t total = 0;
+    for (int gi = 0; gi < G; gi++) total += ((hi[gi] - lo[gi]) + 255) & ~255ull;
+    size_t mfree = 0, mtot = 0;
+    cudaMemGetInfo(&mfree, &mtot);
+    const bool all_slots = total <= mfree / 4;
+    const int R = all_slots ? G : std::min(kSeqSlots, G);
+    if (!s->copy_in) GSV_CUDA(cudaStreamCreateWithFlags(&s->copy_in, cudaStreamNonBlocking));
+    while ((int)s->ev_up.size() < R) {
+        cudaEvent_t e;
+        GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->ev_up.push_back(e);
+    }
+    while ((int)s->ev_slot_done.size() < kSeqSlots * 32) {
+        cudaEvent_t e;
+        GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->ev_slot_done.push_back(e);
+    }
+    std::vector<DevBuf> slot(R);
+    for (int r = 0; r < R; r++)
+        if (int rc = slot[r].alloc((all_slots ? hi[r] - lo[r] : slot_bytes) + 64)) return rc;
+    // the pinned staging of the deferred opens is reset once, with the
+    // session stream drained (nothing of an earlier call still reads it)
+    GSV_CUDA(cudaStreamSynchronize(s->stream));
+    t_stage.reset();
+    for (int attempt = 0; attempt < 4; attempt++) {
+        if (int rc = ensure_aux(s, nstreams, img8, true)) return rc;
+        VideoList vids;
+        int err = GSV_OK;
+        int64_t fo = 0;
+        auto upload_group = [&](int gi) -> int {
+            const int r = gi % R;
+            if (gi >= R)  // ring: the slot's previous group has rendered
+                for (int i = 0; i < nstreams; i++)
+                    GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 32 + i], 0));
+            GSV_CUDA(cudaMemcpyAsync(slot[r].as<uint8_t>(), data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
+                                     s->copy_in));
+            GSV_CUDA(cudaEventRecord(s->ev_up[r], s->copy_in));
+            return GSV_OK;
+        };
+        // descriptors of every group first (small copies that must not queue
+        // behind the payload uploads in the copy engine; a group's device
+        // addresses are its slot's), then the payload uploads -- all of them
+        // when every group has a slot, else each one in the loop once its ring
+        // slot is free
+        for (int gi = 0; gi < G && !err; gi++) {
+            gsv_video* v = nullptr;
+            const std::vector<int> one{sel[gi]};
+            err = open_video(s, data, len, slot[gi % R].as<uint8_t>() - lo[gi], k, &v, &one, true, true);
+            if (!err) vids.v.push_back(v);
+        }
+        if (all_slots)
+            for (int gi = 0; gi < G && !err; gi++) err = upload_group(gi);
+        for (int gi = 0; gi < G && !err; gi++) {
+            const int r = gi % R;
+            if (!all_slots && (err = upload_group(gi))) break;
+            GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
+            gsv_video* v = vids.v[gi];
+            if ((err = v->runs.launch(s->stream, true))) break;
+            std::vector<int32_t> fr((size_t)v->frame_total);
+            for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
+            err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, nullptr, nullptr, host_rgb8 + fo, nstreams,
+                                 (int)(fo % nstreams));
+            if (err) break;
+            if (!all_slots)
+                for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 32 + i], s->aux[i]));
+            fo += v->frame_total;
+        }
+        // drain everything before any buffer goes back to the pool
+        const int jr = join_aux(s, nstreams, true);
+        cudaStreamSynchronize(s->copy_in);
+        const cudaError_t se = cudaStreamSynchronize(s->stream);
+        if (err) return err;
+        if (jr) return jr;
+        if (se != cudaSuccess) return fail(GSV_E_CUDA, std::string("render pipeline: ") + cudaGetErrorString(se));
+        for (gsv_video* v : vids.v) {
+            v->runs.fetch_crc();
+            if (int rc = finish_open(v)) return rc;  // groups in decode order: the first error
+        }
+        const int64_t need = aux_key_overflow(s, nstreams);
+        if (need == 0) {
+            if (frames_out) *frames_out = fo;
+            return GSV_OK;
+        }
+        s->kcap_hint = need + need / 4 + 1024;  // grow and run the sequence again
     }
     return fail(GSV_E_NOMEM, "tile key buffer could not be sized");
 }

@@ -172,6 +172,8 @@ struct RenderWork {
     uint64_t* dkey[2] = {nullptr, nullptr};  // depth sort keys (ping-pong)
     uint32_t* didx[2] = {nullptr, nullptr};  // splat indices (ping-pong)
     SplatRec* rec = nullptr;                 // by splat index
+    uint2* rect = nullptr;                   // (rx, ry) of rec, by splat index: the compact copy
+                                             // the binning / key-emission gathers read
     uint64_t* tie_k = nullptr;               // depth tie fix-up of long runs: key scratch
     uint32_t* tie_runs = nullptr;            // long runs of equal truncated keys (start, end)
     // per key

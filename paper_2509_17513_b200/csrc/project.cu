@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
                                                       uint64_t* __restrict__ dkey,
                                                       uint32_t* __restrict__ didx,
                                                       SplatRec* __restrict__ rec,
+                                                      uint2* __restrict__ rect,
                                                       unsigned long long* __restrict__ ctr,
                                                       int32_t* __restrict__ dbg_rect,
                                                       double* __restrict__ dbg_depth) {
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
             r.rx = (uint32_t)o.x0 | ((uint32_t)o.x1 << 16);
             r.ry = (uint32_t)o.y0 | ((uint32_t)o.y1 << 16);
             rec[i] = r;
+            rect[i] = make_uint2(r.rx, r.ry);
             ntile = rect_tiles(r.rx, r.ry);
         }
         if (dbg_rect) {
@@ -404,7 +406,7 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
         if (smem > 48 * 1024)                                                                       \
             cudaFuncSetAttribute(project_kernel<Loader, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                  (int)smem);                                                        \
-        project_kernel<Loader, D><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, \
+        project_kernel<Loader, D><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, w->rect, \
                                                             w->ctr, dbg_rect, dbg_depth);           \
     } while (0)
     switch (sh_degree) {
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
                                                       const double* __restrict__ colors,
                                                       const double* __restrict__ opac, CamDev cam,
                                                       uint64_t* __restrict__ dkey, uint32_t* __restrict__ didx,
-                                                      SplatRec* __restrict__ rec,
+                                                      SplatRec* __restrict__ rec, uint2* __restrict__ rect,
                                                       unsigned long long* __restrict__ ctr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = false;
@@ -486,6 +488,7 @@ __global__ void __launch_bounds__(128) splat2d_kernel(int64_t n, const double* _
             r.rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
             r.ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
             rec[i] = r;
+            rect[i] = make_uint2(r.rx, r.ry);
             ntile = rect_tiles(r.rx, r.ry);
         }
         dkey[i] = key;
@@ -513,7 +516,7 @@ void launch_splat2d(const Splat2DSrc& src, const CamDev& cam, RenderWork* w, cud
     if (src.n <= 0) return;
     splat2d_kernel<<<(unsigned)((src.n + 127) / 128), 128, 0, s>>>(src.n, src.means, src.cov, src.depth,
                                                                    src.colors, src.opac, cam, w->dkey[0],
-                                                                   w->didx[0], w->rec, w->ctr);
+                                                                   w->didx[0], w->rec, w->rect, w->ctr);
 }
 
 // ---------------------------------------------------------------------------

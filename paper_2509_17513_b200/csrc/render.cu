@@ -370,7 +370,7 @@ __device__ __forceinline__ uint32_t mask_count(const uint32_t* m, uint32_t lo, u
 constexpr int kMaskWordsSmem = 2048;  // open-tile masks of up to 65536 tiles live in shared memory
 
 __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
-    const SplatRec* __restrict__ rec, const uint32_t* __restrict__ didx0, const uint32_t* __restrict__ didx1,
+    const uint2* __restrict__ rect, const uint32_t* __restrict__ didx0, const uint32_t* __restrict__ didx1,
     unsigned long long* __restrict__ ctr, uint32_t a, uint32_t b,
     const uint32_t* __restrict__ open_mask, int ntiles, uint32_t* __restrict__ tkey,
     uint32_t* __restrict__ tval, uint64_t cap, int ntx, unsigned long long* __restrict__ status,
@@ -417,8 +417,7 @@ __global__ void __launch_bounds__(kEmitThreads) round_emit_fused(
     uint32_t sidx = 0;
     if (base < m) {
         sidx = __ldg(order + a + base);
-        const SplatRec* sr = rec + sidx;
-        const uint2 r = make_uint2(__ldg(&sr->rx), __ldg(&sr->ry));
+        const uint2 r = __ldg(rect + sidx);
         x0 = (r.x & 0xFFFFu) / kTile;
         x1 = ((r.x >> 16) - 1) / kTile;
         y0 = (r.y & 0xFFFFu) / kTile;
@@ -530,16 +529,17 @@ __global__ void keys_to_off_kernel(const uint32_t* __restrict__ key, const unsig
 // in rank order and places each splat index at its tiles' next slot.  The
 // compositor then reads each tile's range directly (no tile keys, no search).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void rect_tiles_of(const SplatRec* __restrict__ rec, uint32_t idx, uint32_t& tx0,
+__device__ __forceinline__ void rect_tiles_of(const uint2* __restrict__ rect, uint32_t idx, uint32_t& tx0,
                                               uint32_t& tx1, uint32_t& ty0, uint32_t& ty1) {
-    const uint32_t rx = __ldg(&rec[idx].rx), ry = __ldg(&rec[idx].ry);
+    const uint2 rr = __ldg(rect + idx);
+    const uint32_t rx = rr.x, ry = rr.y;
     tx0 = (rx & 0xFFFFu) / kTile;
     tx1 = ((rx >> 16) - 1) / kTile;
     ty0 = (ry & 0xFFFFu) / kTile;
     ty1 = ((ry >> 16) - 1) / kTile;
 }
 
-__global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restrict__ rec,
+__global__ void __launch_bounds__(256) r1_count_kernel(const uint2* __restrict__ rect,
                                                        const uint32_t* __restrict__ didx0,
                                                        const uint32_t* __restrict__ didx1,
                                                        const unsigned long long* __restrict__ ctr, uint32_t a,
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256) r1_count_kernel(const SplatRec* __restric
     const uint32_t r0 = a + blockIdx.x * B, r1 = min(r0 + B, hi);
     for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
         uint32_t tx0, tx1, ty0, ty1;
-        rect_tiles_of(rec, __ldg(order + r), tx0, tx1, ty0, ty1);
+        rect_tiles_of(rect, __ldg(order + r), tx0, tx1, ty0, ty1);
         for (uint32_t ty = ty0; ty <= ty1; ty++)
             for (uint32_t tx = tx0; tx <= tx1; tx++) {
                 const uint32_t t = ty * (uint32_t)ntx + tx;
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(1024) r1_scan_tiles_kernel(uint32_t* __restric
 
 // one warp per block of ranks: splats in rank order, each one's tiles
 // spread over the lanes; a tile's next slot lives in shared memory
-__global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restrict__ rec,
+__global__ void __launch_bounds__(256) r1_place_kernel(const uint2* __restrict__ rect,
                                                       const uint32_t* __restrict__ didx0,
                                                       const uint32_t* __restrict__ didx1,
                                                       const unsigned long long* __restrict__ ctr, uint32_t a,
@@ -695,8 +695,9 @@ __global__ void __launch_bounds__(256) r1_place_kernel(const SplatRec* __restric
         nrx = nry = 0;
         if (rr < r1) {
             nidx = __ldg(order + rr);
-            nrx = __ldg(&rec[nidx].rx);
-            nry = __ldg(&rec[nidx].ry);
+            const uint2 q = __ldg(rect + nidx);
+            nrx = q.x;
+            nry = q.y;
         }
     };
     if (r0 < r1) fetch(r0);
@@ -753,6 +754,7 @@ void work_free(RenderWork* w) {
         free_ptr(w->tval[b]);
     }
     free_ptr(w->rec);
+    free_ptr(w->rect);
     free_ptr(w->tie_k);
     free_ptr(w->tie_runs);
     free_ptr(w->state);
@@ -786,6 +788,8 @@ int work_reserve(RenderWork* w, int64_t n, int64_t k, int tiles, int64_t npix) {
         }
         free_ptr(w->rec);
         GSV_CUDA(cudaMalloc(&w->rec, c * sizeof(SplatRec)));
+        free_ptr(w->rect);
+        GSV_CUDA(cudaMalloc(&w->rect, c * sizeof(uint2)));
         free_ptr(w->tie_k);
         free_ptr(w->tie_runs);
         GSV_CUDA(cudaMalloc(&w->tie_k, c * sizeof(uint64_t)));
@@ -1078,13 +1082,13 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             if (rc) return rc;
             const size_t sm = (size_t)ntiles * 4;
             if (int rc = r1_smem_attr(sm)) return rc;
-            r1_count_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, mask,
+            r1_count_kernel<<<nblk, 256, sm, s>>>(w->rect, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, mask,
                                                   w->r1_bc);
             r1_scan_blocks_kernel<<<(ntiles + 31) / 32, 32 * ((nblk + 31) / 32), 0, s>>>(w->r1_bc, (int)nblk, ntiles,
                                                                                           w->r1_off);
             r1_scan_tiles_kernel<<<1, 1024, 0, s>>>(w->r1_off, ntiles, ctr, (uint64_t)w->cap_k);
             prof_mark(ST_TSORT, s);
-            r1_place_kernel<<<nblk, 256, sm, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc,
+            r1_place_kernel<<<nblk, 256, sm, s>>>(w->rect, w->didx[0], w->didx[1], ctr, a, b, B, ntx, ntiles, w->r1_bc,
                                                  w->r1_off, w->tval[0], (uint64_t)w->cap_k, mask);
             count_launch(4);
             keys = nullptr;
@@ -1092,7 +1096,7 @@ static int render_enqueue(int64_t n, const CamDev& cam, RenderWork* w, Proj proj
             toff = w->r1_off;
         } else {
             if (!(skip & 8))
-                round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rec, w->didx[0], w->didx[1], ctr, a, b, mask, ntiles,
+                round_emit_fused<<<ge, kEmitThreads, 0, s>>>(w->rect, w->didx[0], w->didx[1], ctr, a, b, mask, ntiles,
                                                            w->tkey[0], w->tval[0], (uint64_t)w->cap_k, ntx, w->status,
                                                            w->ticket, ++w->epoch, th, tp);
             count_launch(1);

@@ -1,0 +1,78 @@
+"""render_sequence (gsv_render_sequence_host): the reference's decode_video
++ render_set + write_ppm of every frame (pipeline.py:350-359,
+render.py:382-385, 165-169) as one pipelined call.  Its u8 frames must equal
+the per-frame path's (DeviceVideo.render with the u8 output) bit for bit,
+for raw containers (the per-group upload/open/render pipeline) and
+range-coded ones (one open of every group), for every prefix, for group
+lists, and a corrupt payload must raise the error decode_video raises."""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import camera, container, scene_names
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gsvb():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2509_17513_b200 as m
+    return m
+
+
+def _per_frame(gsvb, data, k, cam, groups=None):
+    info = gsvb.read_structure(data)
+    gl = list(range(len(info.groups))) if groups is None else list(groups)
+    out = []
+    with gsvb.DeviceVideo(data, k, group_list=gl) as v:
+        for t in range(v.frame_count):
+            u8 = torch.empty((cam.height, cam.width, 3), dtype=torch.uint8, device="cuda")
+            v.render(t, cam, out_u8=u8)
+            out.append(u8.cpu())
+    return torch.stack(out)
+
+
+@pytest.mark.parametrize("name", scene_names())
+def test_sequence_matches_per_frame_render(gsvb, name):
+    data = container(name)
+    cam = camera(name, "oblique")
+    L = gsvb.read_structure(data).layer_count
+    for k in sorted({1, L}):
+        got = gsvb.render_sequence(data, cam, up_to_layer=k)
+        ref = _per_frame(gsvb, data, k, cam)
+        assert got.shape == ref.shape
+        assert torch.equal(got, ref), (name, k)
+
+
+def test_sequence_group_list_and_pinned_source(gsvb):
+    """Groups in any order, from a pinned host tensor."""
+    import bench
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    spec = benchmark_spec(20_000, 12, 3)  # 4 raw groups
+    blobs = encode_stream(lambda: iter_frames(spec, 7), EncodeConfig(layer_count=3, prune_fraction=0.0),
+                          codecs=(0, 1))
+    cam = bench.camera(type("A", (), {"width": 320, "height": 240})())
+    for codec in (0, 1):
+        data = blobs[codec]
+        host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+        for gl in ([0, 1, 2, 3], [2, 0, 3]):
+            got = gsvb.render_sequence(host, cam, up_to_layer=2, groups=gl)
+            ref = _per_frame(gsvb, data, 2, cam, gl)
+            assert torch.equal(got, ref), (codec, gl)
+
+
+def test_sequence_corrupt_payload_raises_like_decode_video(gsvb):
+    from paper_2509_17513_b200.errors import CodecError
+    data = bytearray(container("s1_raw"))
+    info = gsvb.read_structure(bytes(data))
+    e = info.groups[-1].channels[0][0]  # last group: the pipeline has rendered earlier groups
+    data[e.offset + e.size // 2] ^= 0x5A
+    cam = camera("s1_raw", "axis")
+    with pytest.raises(CodecError) as a:
+        gsvb.decode_video(bytes(data))
+    with pytest.raises(CodecError) as b:
+        gsvb.render_sequence(bytes(data), cam)
+    assert str(a.value) == str(b.value)

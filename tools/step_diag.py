@@ -52,11 +52,19 @@ def render_only():
 
 
 def render30():
-    vopen.render_batch(list(range(30)), cs, outs=outs, verify=False)
+    vopen.render_batch(list(range(30)), cs, outs=outs[:30], verify=False)
+
+
+hsrc = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+pinned = torch.empty((300, 1080, 1920, 3), dtype=torch.uint8).pin_memory()
+
+
+def seq_e2e():
+    g.render_sequence(hsrc, cs, up_to_layer=6, out=pinned, session=sess, info=info)
 
 
 for name, fn in (("full", full), ("open", open_only), ("render", render_only), ("render30", render30),
-                 ("full", full)):
+                 ("seq_e2e", seq_e2e), ("full", full)):
     for _ in range(2):
         fn()
     torch.cuda.synchronize()
