@@ -49,6 +49,8 @@ struct gsv_session {
     // of device slots; per slot an "uploaded" event and per (slot, aux
     // stream) a "rendered" event
     cudaStream_t copy_in = nullptr;
+    cudaStream_t check = nullptr;  // the groups' CRC kernels (validation, off the render path)
+    cudaEvent_t ev_prep = nullptr;
     std::vector<cudaEvent_t> ev_up, ev_slot_done;
 };
 
@@ -152,6 +154,38 @@ struct PinnedStage {
 };
 thread_local PinnedStage t_stage;
 
+// Zero-copy descriptor uploads (gsv_render_sequence_host): the copy engine
+// runs host-to-device copies in submission order, so a small descriptor
+// upload enqueued after a group's multi-hundred-MB payload upload would wait
+// for it.  With this flag set, upload() has a kernel read the pinned staging
+// buffer over PCIe instead (UVA: pinned host memory is device-addressable),
+// and memsets are kernels too, so the copy engine carries payloads only.
+thread_local bool t_zero_copy = false;
+
+__global__ void stage_copy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+    const size_t n16 = n / 16;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = n16 * 16 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+__global__ void zero_kernel(uint32_t* __restrict__ p, size_t words) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = 0u;
+}
+int zero_async(void* p, size_t bytes, cudaStream_t s) {  // bytes: a multiple of 4
+    if (!t_zero_copy) {
+        GSV_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+        return GSV_OK;
+    }
+    zero_kernel<<<(unsigned)std::min<size_t>((bytes / 4 + 255) / 256, 148), 256, 0, s>>>(
+        reinterpret_cast<uint32_t*>(p), bytes / 4);
+    count_launch();
+    GSV_CUDA(cudaGetLastError());
+    return GSV_OK;
+}
+
 template <class T>
 int upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
     int rc = b.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
@@ -159,7 +193,13 @@ int upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
     if (v.empty()) return GSV_OK;
     const size_t n = v.size() * sizeof(T);
     uint8_t* h = t_stage.reserve(n, s);
-    if (h) {
+    if (h && t_zero_copy) {  // staging and device blocks are 256-B aligned
+        memcpy(h, v.data(), n);
+        stage_copy_kernel<<<(unsigned)std::min<size_t>((n / 16 + 255) / 256 + 1, 148), 256, 0, s>>>(
+            reinterpret_cast<uint8_t*>(b.p), h, n);
+        count_launch();
+        GSV_CUDA(cudaGetLastError());
+    } else if (h) {
         memcpy(h, v.data(), n);
         GSV_CUDA(cudaMemcpyAsync(b.p, h, n, cudaMemcpyHostToDevice, s));
     } else {
@@ -368,7 +408,7 @@ struct RunSet {
         if ((rc = upload(d_rc, rc_all, s))) return rc;
         if ((rc = upload(d_chunk, chunk_prefix, s))) return rc;
         if ((rc = d_crc.alloc(std::max<size_t>(runs.size(), 1) * 4))) return rc;
-        GSV_CUDA(cudaMemsetAsync(d_crc.p, 0, std::max<size_t>(runs.size(), 1) * 4, s));
+        if ((rc = zero_async(d_crc.p, std::max<size_t>(runs.size(), 1) * 4, s))) return rc;
         for (int b = 0; b < 3; b++) n_cls[b] = (int)rc_runs[b].size();
         nchunks = chunk_prefix.back();
         return GSV_OK;
@@ -376,11 +416,20 @@ struct RunSet {
     // the decode kernels (copy of RAW planes, range decode, CRC) and the CRC
     // read-back; the payload bytes must be on the device by now (stream order)
     int launch(cudaStream_t s, bool deferred) {
+        launch_planes(s);
+        return launch_check(s, deferred);
+    }
+    // what rendering needs: RAW planes of range-coded runs copied to aligned
+    // storage, range-coded planes decoded
+    void launch_planes(cudaStream_t s) {
         prof_mark(ST_RCDEC, s);
         launch_copy_planes(d_jobs.as<CopyJob>(), (int)jobs.size(), s);
         if (!jobs.empty()) count_launch();
         launch_rc_decode(d_runs.as<RunDesc>(), d_rc.as<uint32_t>(), n_cls, d_planes.as<PlaneRef>(), s);
         if (n_cls[0] + n_cls[1] + n_cls[2]) count_launch();
+    }
+    // validation only: the CRC of every run and its read-back
+    int launch_check(cudaStream_t s, bool deferred) {
         prof_mark(ST_CRC, s);
         launch_crc(d_runs.as<RunDesc>(), d_planes.as<PlaneRef>(), (int)planes.size(),
                    d_chunk.as<uint32_t>(), nchunks, d_crc.as<uint32_t>(), s);
@@ -738,6 +787,11 @@ void gsv_session_destroy(gsv_session* s) {
         cudaStreamSynchronize(s->copy_in);
         cudaStreamDestroy(s->copy_in);
     }
+    if (s->check) {
+        cudaStreamSynchronize(s->check);
+        cudaStreamDestroy(s->check);
+    }
+    if (s->ev_prep) cudaEventDestroy(s->ev_prep);
     for (cudaEvent_t e : s->ev_up) cudaEventDestroy(e);
     for (cudaEvent_t e : s->ev_slot_done) cudaEventDestroy(e);
     work_free(&s->work);
@@ -1086,15 +1140,18 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
     for (int gi = 0; gi < G; gi++) total += ((hi[gi] - lo[gi]) + 255) & ~255ull;
     size_t mfree = 0, mtot = 0;
     cudaMemGetInfo(&mfree, &mtot);
-    const bool all_slots = total <= mfree / 4;
+    const char* ring_env = getenv("GSV_SEQ_RING");  // tests: force the ring of slots
+    const bool all_slots = total <= mfree / 4 && !(ring_env && atoi(ring_env) != 0);
     const int R = all_slots ? G : std::min(kSeqSlots, G);
     if (!s->copy_in) GSV_CUDA(cudaStreamCreateWithFlags(&s->copy_in, cudaStreamNonBlocking));
+    if (!s->check) GSV_CUDA(cudaStreamCreateWithFlags(&s->check, cudaStreamNonBlocking));
+    if (!s->ev_prep) GSV_CUDA(cudaEventCreateWithFlags(&s->ev_prep, cudaEventDisableTiming));
     while ((int)s->ev_up.size() < R) {
         cudaEvent_t e;
         GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         s->ev_up.push_back(e);
     }
-    while ((int)s->ev_slot_done.size() < kSeqSlots * 32) {
+    while ((int)s->ev_slot_done.size() < kSeqSlots * 33) {
         cudaEvent_t e;
         GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         s->ev_slot_done.push_back(e);
@@ -1106,52 +1163,110 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
     // session stream drained (nothing of an earlier call still reads it)
     GSV_CUDA(cudaStreamSynchronize(s->stream));
     t_stage.reset();
+    // dev: GSV_DEBUG_SEQ_TIMING=1 prints a per-group timeline (CUDA events)
+    static const bool dbg = getenv("GSV_DEBUG_SEQ_TIMING") != nullptr;
+    struct Mark {
+        const char* what;
+        int g;
+        cudaEvent_t e;
+        double host_ms;
+    };
+    std::vector<Mark> marks;
+    const auto h0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, int g, cudaStream_t st) {
+        if (!dbg) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        marks.push_back({what, g, e, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count()});
+    };
     for (int attempt = 0; attempt < 4; attempt++) {
         if (int rc = ensure_aux(s, nstreams, img8, true)) return rc;
         VideoList vids;
+        mark("start", -1, s->stream);
         int err = GSV_OK;
         int64_t fo = 0;
         auto upload_group = [&](int gi) -> int {
             const int r = gi % R;
             if (gi >= R)  // ring: the slot's previous group has rendered
                 for (int i = 0; i < nstreams; i++)
-                    GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 32 + i], 0));
+                    GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + i], 0));
+            if (gi >= R) GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + 32], 0));
             GSV_CUDA(cudaMemcpyAsync(slot[r].as<uint8_t>(), data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
                                      s->copy_in));
             GSV_CUDA(cudaEventRecord(s->ev_up[r], s->copy_in));
+            mark("uploaded", gi, s->copy_in);
             return GSV_OK;
         };
-        // descriptors of every group first (small copies that must not queue
-        // behind the payload uploads in the copy engine; a group's device
-        // addresses are its slot's), then the payload uploads -- all of them
-        // when every group has a slot, else each one in the loop once its ring
-        // slot is free
+        // every payload upload first when every group has a slot (the copy
+        // engine streams the container from t = 0), else each one in the loop
+        // once its ring slot is free; a group's descriptors go up by zero-copy
+        // kernels on the session stream (never queued behind a payload), just
+        // before the group's kernels
+        // (all groups' descriptor kernels run at the start, while group 0's
+        // payload is still uploading: a later group's kernels would otherwise
+        // queue for SMs behind the renders of the groups before it, and its
+        // frames could not start until those drained)
+        if (all_slots)
+            for (int gi = 0; gi < G && !err; gi++) err = upload_group(gi);
+        t_zero_copy = true;
         for (int gi = 0; gi < G && !err; gi++) {
             gsv_video* v = nullptr;
             const std::vector<int> one{sel[gi]};
             err = open_video(s, data, len, slot[gi % R].as<uint8_t>() - lo[gi], k, &v, &one, true, true);
             if (!err) vids.v.push_back(v);
         }
-        if (all_slots)
-            for (int gi = 0; gi < G && !err; gi++) err = upload_group(gi);
+        t_zero_copy = false;
+        // the CRC stream sees every group's descriptors and zeroed CRC slots
+        if (!err) {
+            GSV_CUDA(cudaEventRecord(s->ev_prep, s->stream));
+            GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_prep, 0));
+        }
+        mark("prepared", -1, s->stream);
         for (int gi = 0; gi < G && !err; gi++) {
             const int r = gi % R;
+            gsv_video* v = vids.v[gi];
             if (!all_slots && (err = upload_group(gi))) break;
             GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
-            gsv_video* v = vids.v[gi];
-            if ((err = v->runs.launch(s->stream, true))) break;
+            // renders fork before the group's CRC (validation only): they never
+            // wait for the CRC kernel, which runs as SM resources free up
+            v->runs.launch_planes(s->stream);
+            mark("fork", gi, s->stream);
             std::vector<int32_t> fr((size_t)v->frame_total);
             for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
             err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, nullptr, nullptr, host_rgb8 + fo, nstreams,
                                  (int)(fo % nstreams));
             if (err) break;
-            if (!all_slots)
-                for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 32 + i], s->aux[i]));
+            for (int i = 0; i < nstreams && dbg; i++) mark("rendered", gi, s->aux[i]);
+            for (int i = 0; i < nstreams && dbg; i++) mark("copied", gi, s->aux_copy[i]);
+            // the group's CRC on its own stream: no render or later open waits for it
+            GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_up[r], 0));
+            if ((err = v->runs.launch_check(s->check, true))) break;
+            if (!all_slots) {  // the slot is free once the group has rendered and its CRC has run
+                for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 33 + i], s->aux[i]));
+                GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 33 + 32], s->check));
+            }
             fo += v->frame_total;
         }
         // drain everything before any buffer goes back to the pool
         const int jr = join_aux(s, nstreams, true);
+        mark("joined", -1, s->stream);
+        mark("checked", -1, s->check);
         cudaStreamSynchronize(s->copy_in);
+        cudaStreamSynchronize(s->check);
+        if (dbg) fprintf(stderr, "[seq] host: synced copy+check at %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+        if (dbg) {
+            cudaDeviceSynchronize();
+            for (const Mark& m : marks) {
+                float t = 0;
+                cudaEventElapsedTime(&t, marks[0].e, m.e);
+                fprintf(stderr, "[seq] %-9s g%-3d gpu %8.3f ms  host-enqueued %8.3f ms\n", m.what, m.g, t, m.host_ms);
+            }
+            for (const Mark& m : marks) cudaEventDestroy(m.e);
+            marks.clear();
+            cudaGetLastError();
+        }
         const cudaError_t se = cudaStreamSynchronize(s->stream);
         if (err) return err;
         if (jr) return jr;
@@ -1160,6 +1275,8 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
             v->runs.fetch_crc();
             if (int rc = finish_open(v)) return rc;  // groups in decode order: the first error
         }
+        if (dbg) fprintf(stderr, "[seq] host: checked at %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
         const int64_t need = aux_key_overflow(s, nstreams);
         if (need == 0) {
             if (frames_out) *frames_out = fo;

@@ -271,18 +271,25 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
             // strip rows against the rect: warp-uniform skip (a strip of 8-row
             // lanes is the whole tile: every record overlaps it)
             if (kStrips > 1 && ((mw >> (16 + strip * 2 * ROWS)) & ((1u << (2 * ROWS)) - 1u)) == 0u) continue;
+            // V3: the rect covers all 16 rows of the tile (row mask 0xFFFF;
+            // warp-uniform).  Such records skip the vote below: it finds
+            // nothing to skip for ~97% of them, and its reduction sits on the
+            // record's dependency chain
+            const bool full = V3 && mw >= 0xFFFF0000u;
             // rows of the lane's column inside the rect (empty outside its columns)
-            uint32_t m;
-            if constexpr (V3) {
-                m = (mw & colbit) ? __byte_perm(mw, 0u, rsel) : 0u;
-            } else {
-                m = ((mw >> colsh) & 1u) ? (mw >> rowsh) & ((1u << ROWS) - 1u) : 0u;
+            uint32_t m = 0u, need = 0xFFu;
+            if (!full) {
+                if constexpr (V3) {
+                    m = (mw & colbit) ? __byte_perm(mw, 0u, rsel) : 0u;
+                } else {
+                    m = ((mw >> colsh) & 1u) ? (mw >> rowsh) & ((1u << ROWS) - 1u) : 0u;
+                }
+                // rows some lane still needs (rect and T >= 1e-4): one vote per
+                // record, then whole row pairs no lane needs are skipped with a
+                // warp-uniform branch (rect edges, saturated rows)
+                need = __reduce_or_sync(0xffffffffu, m & live);
+                if (!need) continue;
             }
-            // rows some lane still needs (rect and T >= 1e-4): one vote per
-            // record, then whole row pairs no lane needs are skipped with a
-            // warp-uniform branch (rect edges, saturated rows)
-            const uint32_t need = __reduce_or_sync(0xffffffffu, m & live);
-            if (!need) continue;
             float4 a, r3;
             if constexpr (V3) {
                 float2 cab;
@@ -311,8 +318,6 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
                 // 0.99, no 0.99 cap (alpha <= op); the reference's p = min(p,
                 // 0) only trims rounding (the conic is positive definite)
                 float A1 = TEFF ? A + __uint_as_float(__float_as_uint(r3.w)) : A;
-                // V3: the rect covers all 16 rows of the tile (row mask 0xFFFF)
-                const bool full = V3 && mw >= 0xFFFF0000u;
                 if (V3 && !(mw & colbit)) A1 = -INFINITY;
                 const f2 A2{A1, A1}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
                 const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};

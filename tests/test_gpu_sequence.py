@@ -46,19 +46,23 @@ def test_sequence_matches_per_frame_render(gsvb, name):
         assert torch.equal(got, ref), (name, k)
 
 
-def test_sequence_group_list_and_pinned_source(gsvb):
-    """Groups in any order, from a pinned host tensor."""
+@pytest.mark.parametrize("ring", ["0", "1"])
+def test_sequence_group_list_and_pinned_source(gsvb, ring, monkeypatch):
+    """Groups in any order, from a pinned host tensor; every group in its own
+    device slot, or (GSV_SEQ_RING=1) the ring of 3 slots reused as groups
+    finish."""
+    monkeypatch.setenv("GSV_SEQ_RING", ring)
     import bench
     from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
     from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
-    spec = benchmark_spec(20_000, 12, 3)  # 4 raw groups
+    spec = benchmark_spec(20_000, 15, 3)  # 5 raw groups: the ring wraps
     blobs = encode_stream(lambda: iter_frames(spec, 7), EncodeConfig(layer_count=3, prune_fraction=0.0),
                           codecs=(0, 1))
     cam = bench.camera(type("A", (), {"width": 320, "height": 240})())
     for codec in (0, 1):
         data = blobs[codec]
         host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
-        for gl in ([0, 1, 2, 3], [2, 0, 3]):
+        for gl in ([0, 1, 2, 3, 4], [2, 0, 4, 3]):
             got = gsvb.render_sequence(host, cam, up_to_layer=2, groups=gl)
             ref = _per_frame(gsvb, data, 2, cam, gl)
             assert torch.equal(got, ref), (codec, gl)

@@ -1,0 +1,5 @@
+set -x
+O=gpurun_out/r2v
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_sequence.py -q -p no:cacheprovider -rf > $O/pytest_seq.log 2>&1
+timeout 900 python tools/e2e_probe.py > $O/e2e_probe.txt 2>&1
