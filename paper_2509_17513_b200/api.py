@@ -476,8 +476,8 @@ def decode_video(source, up_to_layer: int | None = None) -> DecodedVideo:
 
 
 def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, out: torch.Tensor | None = None,
-                    streams: int = 8, session: Session | None = None, info: ContainerInfo | None = None
-                    ) -> torch.Tensor:
+                    streams: int = 8, session: Session | None = None, info: ContainerInfo | None = None,
+                    resident: torch.Tensor | None = None, outs=None, outs_u8=None):
     """Every frame of a container (or of the listed groups), decoded at
     prefix k and rendered, as u8 RGB in host memory: the reference's
     `decode_video(path, k)` followed by `render_set(video.frame(t), cam)` and
@@ -489,7 +489,12 @@ def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, ou
     source: container bytes or a host uint8 tensor (pinned memory makes the
     uploads asynchronous); out: optional host uint8 tensor (frames, H, W, 3),
     pinned for asynchronous read-back.  Returns `out` (frames in group-list
-    order, group-major)."""
+    order, group-major).
+
+    resident: the whole container already in HBM (a CUDA uint8 tensor;
+    nothing is uploaded); outs / outs_u8: per-frame device tensors (fp32 /
+    u8, (H, W, 3)) instead of the host frames -- then `out` is only filled
+    when given, and None is returned when it is not."""
     s = session or default_session()
     if isinstance(source, torch.Tensor):
         if source.is_cuda or source.dtype != torch.uint8:
@@ -517,18 +522,32 @@ def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, ou
     nfr = sum(int(info.groups[g].frame_count) for g in gl)
     c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
     H, W = int(c.height), int(c.width)
-    if out is None:
+    device_out = outs is not None or outs_u8 is not None
+    if out is None and not device_out:
         out = torch.empty((nfr, H, W, 3), dtype=torch.uint8, pin_memory=torch.cuda.is_available())
-    if out.shape != (nfr, H, W, 3) or out.dtype != torch.uint8 or out.is_cuda or not out.is_contiguous():
-        raise InvalidInputError(f"out must be a contiguous host uint8 tensor of shape {(nfr, H, W, 3)}")
-    base, step = out.data_ptr(), H * W * 3
-    ptrs = (ctypes.c_void_p * max(1, nfr))(*[base + j * step for j in range(nfr)])
+    host_ptrs = None
+    if out is not None:
+        if out.shape != (nfr, H, W, 3) or out.dtype != torch.uint8 or out.is_cuda or not out.is_contiguous():
+            raise InvalidInputError(f"out must be a contiguous host uint8 tensor of shape {(nfr, H, W, 3)}")
+        base, step = out.data_ptr(), H * W * 3
+        host_ptrs = (ctypes.c_void_p * max(1, nfr))(*[base + j * step for j in range(nfr)])
+
+    def dev_arr(ts, dtype):
+        if ts is None:
+            return None
+        if len(ts) != nfr or any(t.dtype != dtype or not t.is_cuda or tuple(t.shape) != (H, W, 3) for t in ts):
+            raise InvalidInputError(f"{nfr} CUDA tensors of shape {(H, W, 3)} and dtype {dtype} expected")
+        return (ctypes.c_void_p * max(1, nfr))(*[t.data_ptr() for t in ts])
+    a_rgb, a_u8 = dev_arr(outs, torch.float32), dev_arr(outs_u8, torch.uint8)
+    if resident is not None and (not resident.is_cuda or resident.dtype != torch.uint8 or resident.numel() < nbytes):
+        raise InvalidInputError("resident must be a CUDA uint8 tensor holding the whole container")
     arr = (ctypes.c_int32 * max(1, len(gl)))(*gl)
     k = -1 if up_to_layer is None else int(up_to_layer)
     written = ctypes.c_int64(0)
     _pre(s)
-    check(s.lib.gsv_render_sequence_host(s.handle, hptr, nbytes, k, arr, len(gl), ctypes.byref(c), ptrs,
-                                         int(streams), ctypes.byref(written)))
+    check(s.lib.gsv_render_sequence(s.handle, hptr, nbytes, resident.data_ptr() if resident is not None else None,
+                                    k, arr, len(gl), ctypes.byref(c), a_rgb, a_u8, host_ptrs, int(streams),
+                                    ctypes.byref(written)))
     _post(s)
     return out
 

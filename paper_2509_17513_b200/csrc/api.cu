@@ -24,6 +24,10 @@
 
 using namespace gsv;
 
+// u8 staging buffers per aux stream for host outputs: the render of frame j
+// on a stream waits for the read-back of frame j - kU8Bufs on it
+constexpr int kU8Bufs = 3;
+
 struct gsv_session {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -34,7 +38,7 @@ struct gsv_session {
     // frame overlap with other frames' kernels
     std::vector<cudaStream_t> aux;
     std::vector<RenderWork*> aux_work;
-    std::vector<uint8_t*> aux_u8;  // staging for host u8 outputs: 2 buffers per aux stream
+    std::vector<uint8_t*> aux_u8;  // staging for host u8 outputs: kU8Bufs buffers per aux stream
     std::vector<size_t> aux_u8_cap;
     // read-back of host u8 outputs: per aux stream a copy stream, and per
     // staging buffer "rendered" / "copied" events, so the D2H of frame j
@@ -52,6 +56,10 @@ struct gsv_session {
     cudaStream_t check = nullptr;  // the groups' CRC kernels (validation, off the render path)
     cudaEvent_t ev_prep = nullptr;
     std::vector<cudaEvent_t> ev_up, ev_slot_done;
+    // the payload slots, kept across calls (grow-only: cudaMalloc / cudaFree
+    // synchronise, so they are not taken from the pool on every call)
+    std::vector<uint8_t*> seq_slot;
+    std::vector<size_t> seq_slot_cap;
 };
 
 namespace {
@@ -128,16 +136,25 @@ struct DevBuf {
 struct PinnedStage {
     uint8_t* p = nullptr;
     size_t cap = 0, used = 0;
+    // outgrown buffers: copies enqueued from them may still be in flight, so
+    // they are freed only at reset(), which callers invoke with the work that
+    // used the stage drained (cudaFreeHost can synchronise the device: never
+    // called while a pipeline is being enqueued)
+    std::vector<uint8_t*> retired;
     ~PinnedStage() {
         if (p) cudaFreeHost(p);
+        for (uint8_t* q : retired) cudaFreeHost(q);
     }
-    void reset() { used = 0; }
-    uint8_t* reserve(size_t n, cudaStream_t s) {
+    void reset() {
+        used = 0;
+        for (uint8_t* q : retired) cudaFreeHost(q);
+        retired.clear();
+    }
+    uint8_t* reserve(size_t n, cudaStream_t) {
         const size_t need = ((used + 255) & ~size_t(255)) + n;
-        if (need > cap) {  // grow: drain in-flight copies from the old buffer first
-            cudaStreamSynchronize(s);
-            if (p) cudaFreeHost(p);
-            cap = std::max(need * 2, (size_t)1 << 20);
+        if (need > cap) {  // grow into a fresh buffer; the old one is retired
+            if (p) retired.push_back(p);
+            cap = std::max(need * 2, (size_t)8 << 20);
             p = nullptr;
             if (cudaMallocHost(reinterpret_cast<void**>(&p), cap) != cudaSuccess) {
                 p = nullptr;
@@ -772,10 +789,10 @@ void gsv_session_destroy(gsv_session* s) {
         cudaStreamSynchronize(s->aux_copy[i]);
         work_free(s->aux_work[i]);
         delete s->aux_work[i];
-        for (int b = 0; b < 2; b++) {
-            if (s->aux_u8[2 * i + b]) cudaFree(s->aux_u8[2 * i + b]);
-            cudaEventDestroy(s->ev_rendered[2 * i + b]);
-            cudaEventDestroy(s->ev_copied[2 * i + b]);
+        for (int b = 0; b < kU8Bufs; b++) {
+            if (s->aux_u8[kU8Bufs * i + b]) cudaFree(s->aux_u8[kU8Bufs * i + b]);
+            cudaEventDestroy(s->ev_rendered[kU8Bufs * i + b]);
+            cudaEventDestroy(s->ev_copied[kU8Bufs * i + b]);
         }
         cudaStreamDestroy(s->aux[i]);
         cudaStreamDestroy(s->aux_copy[i]);
@@ -793,6 +810,8 @@ void gsv_session_destroy(gsv_session* s) {
     }
     if (s->ev_prep) cudaEventDestroy(s->ev_prep);
     for (cudaEvent_t e : s->ev_up) cudaEventDestroy(e);
+    for (uint8_t* p : s->seq_slot)
+        if (p) cudaFree(p);
     for (cudaEvent_t e : s->ev_slot_done) cudaEventDestroy(e);
     work_free(&s->work);
     if (s->own_stream) cudaStreamDestroy(s->stream);
@@ -922,7 +941,7 @@ int ensure_aux(gsv_session* s, int nstreams, size_t img8, bool host_out) {
         GSV_CUDA(cudaEventCreateWithFlags(&cj, cudaEventDisableTiming));
         s->ev_copy_join.push_back(cj);
         s->aux_flip.push_back(0);
-        for (int b = 0; b < 2; b++) {
+        for (int b = 0; b < kU8Bufs; b++) {
             s->aux_u8.push_back(nullptr);
             s->aux_u8_cap.push_back(0);
             cudaEvent_t er, ec;
@@ -940,8 +959,8 @@ int ensure_aux(gsv_session* s, int nstreams, size_t img8, bool host_out) {
             int rc = work_reserve(s->aux_work[i], 1, khint, 0, 0);
             if (rc) return rc;
         }
-        for (int b = 0; b < 2 && host_out; b++) {
-            const int q = 2 * i + b;
+        for (int b = 0; b < kU8Bufs && host_out; b++) {
+            const int q = kU8Bufs * i + b;
             if (s->aux_u8_cap[q] < img8) {
                 GSV_CUDA(cudaStreamSynchronize(s->aux_copy[i]));
                 if (s->aux_u8[q]) cudaFree(s->aux_u8[q]);
@@ -972,8 +991,8 @@ int enqueue_frames(gsv_video* v, const int32_t* frames, int count, const CamDev&
         const bool to_host = host_rgb8 && host_rgb8[j];
         int q = 0;
         if (to_host) {
-            q = 2 * i + s->aux_flip[i];
-            s->aux_flip[i] ^= 1;
+            q = kU8Bufs * i + s->aux_flip[i];
+            s->aux_flip[i] = (s->aux_flip[i] + 1) % kU8Bufs;
             GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_copied[q], 0));  // staging buffer free
             o8 = s->aux_u8[q];
         }
@@ -1079,9 +1098,20 @@ bool group_is_raw(const uint8_t* data, size_t len, const GroupDir& gd, int k) {
 int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer,
                              const int32_t* groups, int ngroups, const gsv_camera* cam,
                              uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
+    if (!host_rgb8) return fail(GSV_E_INVALID_INPUT, "host_rgb8 is NULL");
+    return gsv_render_sequence(s, data, len, nullptr, up_to_layer, groups, ngroups, cam, nullptr, nullptr, host_rgb8,
+                               nstreams, frames_out);
+}
+
+int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data, int up_to_layer,
+                        const int32_t* groups, int ngroups, const gsv_camera* cam, float* const* out_rgb,
+                        uint8_t* const* out_rgb8, uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
+    const auto t_entry = std::chrono::steady_clock::now();
     GSV_CUDA(cudaSetDevice(s->device));
     if (frames_out) *frames_out = 0;
-    if (!host_rgb8) return fail(GSV_E_INVALID_INPUT, "host_rgb8 is NULL");
+    if (!out_rgb && !out_rgb8 && !host_rgb8) return fail(GSV_E_INVALID_INPUT, "no output array given");
+    const bool host_out = host_rgb8 != nullptr;
+    const bool resident = dev_data != nullptr;
     if (cam->width < 1 || cam->height < 1) return fail(GSV_E_INVALID_INPUT, "image dimensions must be >= 1");
     nstreams = std::max(1, std::min(nstreams, 32));
     Container c;
@@ -1106,10 +1136,10 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
 
     if (!raw || sel.size() < 2) {
         gsv_video* v = nullptr;
-        if (int rc = open_video(s, data, len, nullptr, k, &v, &sel)) return rc;
+        if (int rc = open_video(s, data, len, dev_data, k, &v, &sel)) return rc;
         std::vector<int32_t> fr((size_t)v->frame_total);
         for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
-        int rc = gsv_video_render_batch(v, fr.data(), (int)fr.size(), cam, nullptr, nullptr, host_rgb8, nstreams, 1);
+        int rc = gsv_video_render_batch(v, fr.data(), (int)fr.size(), cam, out_rgb, out_rgb8, host_rgb8, nstreams, 1);
         cudaStreamSynchronize(s->stream);
         if (!rc && frames_out) *frames_out = v->frame_total;
         delete v;
@@ -1141,7 +1171,7 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
     size_t mfree = 0, mtot = 0;
     cudaMemGetInfo(&mfree, &mtot);
     const char* ring_env = getenv("GSV_SEQ_RING");  // tests: force the ring of slots
-    const bool all_slots = total <= mfree / 4 && !(ring_env && atoi(ring_env) != 0);
+    const bool all_slots = resident || (total <= mfree / 4 && !(ring_env && atoi(ring_env) != 0));
     const int R = all_slots ? G : std::min(kSeqSlots, G);
     if (!s->copy_in) GSV_CUDA(cudaStreamCreateWithFlags(&s->copy_in, cudaStreamNonBlocking));
     if (!s->check) GSV_CUDA(cudaStreamCreateWithFlags(&s->check, cudaStreamNonBlocking));
@@ -1156,9 +1186,28 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
         GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         s->ev_slot_done.push_back(e);
     }
-    std::vector<DevBuf> slot(R);
-    for (int r = 0; r < R; r++)
-        if (int rc = slot[r].alloc((all_slots ? hi[r] - lo[r] : slot_bytes) + 64)) return rc;
+    if ((int)s->seq_slot.size() < R) {
+        s->seq_slot.resize(R, nullptr);
+        s->seq_slot_cap.resize(R, 0);
+    }
+    for (int r = 0; r < R && !resident; r++) {
+        const size_t want = (all_slots ? hi[r] - lo[r] : slot_bytes) + 64;
+        if (s->seq_slot_cap[r] < want) {
+            if (s->seq_slot[r]) cudaFree(s->seq_slot[r]);
+            s->seq_slot[r] = nullptr;
+            s->seq_slot_cap[r] = 0;
+            const size_t cap = want + want / 8;  // slack: group sizes vary a little between calls
+            if (cudaMalloc(&s->seq_slot[r], cap) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(GSV_E_CUDA, "cudaMalloc: out of memory (sequence payload slots)");
+            }
+            s->seq_slot_cap[r] = cap;
+        }
+    }
+    const std::vector<uint8_t*>& slot = s->seq_slot;
+    // device base address of group gi's payload offsets: its slot (which holds
+    // bytes [lo, hi) of the container), or the resident container itself
+    auto dev_base = [&](int gi) -> const uint8_t* { return resident ? dev_data : slot[gi % R] - lo[gi]; };
     // the pinned staging of the deferred opens is reset once, with the
     // session stream drained (nothing of an earlier call still reads it)
     GSV_CUDA(cudaStreamSynchronize(s->stream));
@@ -1173,6 +1222,8 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
     };
     std::vector<Mark> marks;
     const auto h0 = std::chrono::steady_clock::now();
+    if (dbg) fprintf(stderr, "[seq] host: setup (parse, slots, sync) %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(h0 - t_entry).count());
     auto mark = [&](const char* what, int g, cudaStream_t st) {
         if (!dbg) return;
         cudaEvent_t e;
@@ -1181,7 +1232,7 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
         marks.push_back({what, g, e, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count()});
     };
     for (int attempt = 0; attempt < 4; attempt++) {
-        if (int rc = ensure_aux(s, nstreams, img8, true)) return rc;
+        if (int rc = ensure_aux(s, nstreams, img8, host_out)) return rc;
         VideoList vids;
         mark("start", -1, s->stream);
         int err = GSV_OK;
@@ -1192,7 +1243,7 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
                 for (int i = 0; i < nstreams; i++)
                     GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + i], 0));
             if (gi >= R) GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + 32], 0));
-            GSV_CUDA(cudaMemcpyAsync(slot[r].as<uint8_t>(), data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
+            GSV_CUDA(cudaMemcpyAsync(slot[r], data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
                                      s->copy_in));
             GSV_CUDA(cudaEventRecord(s->ev_up[r], s->copy_in));
             mark("uploaded", gi, s->copy_in);
@@ -1207,40 +1258,52 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
         // payload is still uploading: a later group's kernels would otherwise
         // queue for SMs behind the renders of the groups before it, and its
         // frames could not start until those drained)
-        if (all_slots)
-            for (int gi = 0; gi < G && !err; gi++) err = upload_group(gi);
-        t_zero_copy = true;
-        for (int gi = 0; gi < G && !err; gi++) {
+        // (resident: no payload copies, so the descriptors go by ordinary
+        // copies, group by group, each just before its frames)
+        auto prepare = [&](int gi) -> int {
             gsv_video* v = nullptr;
             const std::vector<int> one{sel[gi]};
-            err = open_video(s, data, len, slot[gi % R].as<uint8_t>() - lo[gi], k, &v, &one, true, true);
-            if (!err) vids.v.push_back(v);
+            const int e = open_video(s, data, len, dev_base(gi), k, &v, &one, true, true);
+            if (!e) vids.v.push_back(v);
+            return e;
+        };
+        if (!resident) {
+            if (all_slots)
+                for (int gi = 0; gi < G && !err; gi++) err = upload_group(gi);
+            t_zero_copy = true;
+            for (int gi = 0; gi < G && !err; gi++) err = prepare(gi);
+            t_zero_copy = false;
+            // the CRC stream sees every group's descriptors and zeroed CRC slots
+            if (!err) {
+                GSV_CUDA(cudaEventRecord(s->ev_prep, s->stream));
+                GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_prep, 0));
+            }
+            mark("prepared", -1, s->stream);
         }
-        t_zero_copy = false;
-        // the CRC stream sees every group's descriptors and zeroed CRC slots
-        if (!err) {
-            GSV_CUDA(cudaEventRecord(s->ev_prep, s->stream));
-            GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_prep, 0));
-        }
-        mark("prepared", -1, s->stream);
         for (int gi = 0; gi < G && !err; gi++) {
             const int r = gi % R;
+            if (resident) {
+                if ((err = prepare(gi))) break;
+                GSV_CUDA(cudaEventRecord(s->ev_prep, s->stream));
+                GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_prep, 0));
+            }
             gsv_video* v = vids.v[gi];
             if (!all_slots && (err = upload_group(gi))) break;
-            GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
+            if (!resident) GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
             // renders fork before the group's CRC (validation only): they never
             // wait for the CRC kernel, which runs as SM resources free up
             v->runs.launch_planes(s->stream);
             mark("fork", gi, s->stream);
             std::vector<int32_t> fr((size_t)v->frame_total);
             for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
-            err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, nullptr, nullptr, host_rgb8 + fo, nstreams,
+            err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, out_rgb ? out_rgb + fo : nullptr,
+                                 out_rgb8 ? out_rgb8 + fo : nullptr, host_rgb8 ? host_rgb8 + fo : nullptr, nstreams,
                                  (int)(fo % nstreams));
             if (err) break;
             for (int i = 0; i < nstreams && dbg; i++) mark("rendered", gi, s->aux[i]);
-            for (int i = 0; i < nstreams && dbg; i++) mark("copied", gi, s->aux_copy[i]);
+            for (int i = 0; i < nstreams && dbg && host_out; i++) mark("copied", gi, s->aux_copy[i]);
             // the group's CRC on its own stream: no render or later open waits for it
-            GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_up[r], 0));
+            if (!resident) GSV_CUDA(cudaStreamWaitEvent(s->check, s->ev_up[r], 0));
             if ((err = v->runs.launch_check(s->check, true))) break;
             if (!all_slots) {  // the slot is free once the group has rendered and its CRC has run
                 for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 33 + i], s->aux[i]));
@@ -1249,7 +1312,7 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
             fo += v->frame_total;
         }
         // drain everything before any buffer goes back to the pool
-        const int jr = join_aux(s, nstreams, true);
+        const int jr = join_aux(s, nstreams, host_out);
         mark("joined", -1, s->stream);
         mark("checked", -1, s->check);
         cudaStreamSynchronize(s->copy_in);

@@ -80,3 +80,27 @@ def test_sequence_corrupt_payload_raises_like_decode_video(gsvb):
     with pytest.raises(CodecError) as b:
         gsvb.render_sequence(bytes(data), cam)
     assert str(a.value) == str(b.value)
+
+
+def test_sequence_resident_device_outputs(gsvb):
+    """The container already in HBM (no uploads), device u8 and fp32 outputs:
+    the path the bench's resident step runs."""
+    import bench
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    spec = benchmark_spec(20_000, 12, 3)
+    blobs = encode_stream(lambda: iter_frames(spec, 11), EncodeConfig(layer_count=3, prune_fraction=0.0),
+                          codecs=(0, 1))
+    cam = bench.camera(type("A", (), {"width": 256, "height": 192})())
+    for codec in (0, 1):
+        data = blobs[codec]
+        dev = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+        ref = _per_frame(gsvb, data, 3, cam)
+        u8 = [torch.empty((192, 256, 3), dtype=torch.uint8, device="cuda") for _ in range(ref.shape[0])]
+        f32 = [torch.empty((192, 256, 3), dtype=torch.float32, device="cuda") for _ in range(ref.shape[0])]
+        assert gsvb.render_sequence(data, cam, up_to_layer=3, resident=dev, outs=f32, outs_u8=u8) is None
+        got = torch.stack([t.cpu() for t in u8])
+        assert torch.equal(got, ref), codec
+        with gsvb.DeviceVideo(data, 3) as v:
+            img = v.render(5, cam)
+        assert torch.equal(f32[5], img)
