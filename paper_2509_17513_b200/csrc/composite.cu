@@ -147,17 +147,27 @@ __device__ __forceinline__ float ex2f(float x) {
 // decision from log2 op; the arithmetic is V2's, op for op (only records
 // with op in (0.98994, 0.99] also take the 0.99 cap, which can only round an
 // alpha of 0.99 + 1 ulp down to the reference's ceiling).
-template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5>
-__global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
+//
+// V4 (CT = true, default): the staging lane also tabulates its record's
+// per-column terms for the 16 columns of the tile -- A_c = dx (ca dx) +
+// log2 op (-inf outside the rect's columns) and B_c = cb dx with dx = c + bx
+// -- and the dy pairs of the two lane halves, so a lane's per-record work is
+// loads: (A, B) of its column, its half's dy pair, (cc, r, g, b), and the
+// mask / log2-op pair.  The arithmetic is V3's, op for op (bit-identical).
+// The table rows are 17 float2 apart (bank-conflict-free both ways).
+template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5, int WPC = 4,
+          bool CT = false>
+__global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >= 5 ? 96 : 128)) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
     int ntiles, bool first, bool last, float bg0, float bg1, float bg2, float* __restrict__ out_rgb,
     uint8_t* __restrict__ out_rgb8) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
-    __shared__ __align__(16) float4 s_rec[2][4][32 * 4];  // double-buffered per-warp batches
+    __shared__ __align__(16) float4 s_rec[2][WPC][32 * 4];  // double-buffered per-warp batches
+    __shared__ __align__(16) float2 s_ct[CT ? WPC : 1][CT ? 32 * 17 : 1];  // V4 column tables
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * 4 + warp;
+    const int gw = blockIdx.x * WPC + warp;
     const int tile = gw / kStrips, strip = gw % kStrips;
     if (tile >= ntiles) return;
     // per-strip state: saturated strips were written out in an earlier round;
@@ -189,6 +199,10 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
     // V3: the lane's column bit and the byte permute that moves its 8 rows of
     // the rect's row mask (mask bits 16-31) to bits 0-7
     const uint32_t colbit = 1u << colsh, rsel = 0x4440u | (rowsh >> 3);
+    // V4: this lane's entry of record 0 in the warp's column table, and the
+    // offset of its half's dy pair in a staged record
+    const uint32_t ct_lane = CT ? (uint32_t)__cvta_generic_to_shared(&s_ct[warp][0]) + 8u * colsh : 0u;
+    const uint32_t dy_off = 16u + 8u * (uint32_t)(lane >> 4);
     float T[ROWS], c0[ROWS], c1[ROWS], c2[ROWS];
     uint32_t live = 0, inimg = 0;
     const bool work = on && start < end;
@@ -216,8 +230,10 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
     // buffered per warp; the rank of the batch after that is loaded a batch
     // ahead too, so neither the rank nor the record gather sits in front of
     // the compositing (round 2's few open tiles are latency-bound)
-    const uint32_t sb[2] = {(uint32_t)__cvta_generic_to_shared(&s_rec[0][warp][0]),
-                            (uint32_t)__cvta_generic_to_shared(&s_rec[1][warp][0])};
+    // the warp's two batch buffers (arithmetic, not an indexed local array)
+    const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(&s_rec[0][warp][0]);
+    constexpr uint32_t kBufStride = (uint32_t)(sizeof(float4) * WPC * 32 * 4);
+    auto sb = [&](int i) { return sb0 + (uint32_t)(i & 1) * kBufStride; };
     auto issue = [&](uint32_t dst, uint32_t jr, uint32_t rank) {
         if (jr < end) {
             const char* src = reinterpret_cast<const char*>(recs + rank);
@@ -230,16 +246,16 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
     };
     uint32_t rank_nx = 0;
     if (work) {
-        issue(sb[0], start + lane, start + lane < end ? __ldg(ranks + start + lane) : 0u);
+        issue(sb(0), start + lane, start + lane < end ? __ldg(ranks + start + lane) : 0u);
         rank_nx = start + 32 + lane < end ? __ldg(ranks + start + 32 + lane) : 0u;
     }
     int it = 0;
     for (uint32_t base = start; work && base < end; base += 32, it++) {
         if (!__any_sync(0xffffffffu, live)) break;
-        const uint32_t sbase = sb[it & 1];
+        const uint32_t sbase = sb(it);
         const bool more = base + 32 < end;
         if (more) {
-            issue(sb[(it + 1) & 1], base + 32 + lane, rank_nx);
+            issue(sb(it + 1), base + 32 + lane, rank_nx);
             rank_nx = base + 64 + lane < end ? __ldg(ranks + base + 64 + lane) : 0u;
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
@@ -259,8 +275,25 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
             const int rl = min(max((int)(ry & 0xFFFFu) - ty0, 0), 16), rh = min(max((int)(ry >> 16) - ty0, 0), 16);
             const uint32_t cm = (0xFFFFu << cl) & ~(0xFFFFu << ch) & 0xFFFFu;
             const uint32_t rm = (0xFFFFu << rl) & ~(0xFFFFu << rh) & 0xFFFFu;
-            sts_f4(sl, make_float4(((float)tx0 - v0.x) - v1.x, ((float)ty0 - v0.y) - v1.y,
-                                   __uint_as_float(cm | (rm << 16)), V3 ? v3.w : 0.f));
+            const float bxv = ((float)tx0 - v0.x) - v1.x, byv = ((float)ty0 - v0.y) - v1.y;
+            sts_f4(sl, make_float4(bxv, byv, __uint_as_float(cm | (rm << 16)), V3 ? v3.w : 0.f));
+            if constexpr (CT) {
+                // the per-lane V3 terms, for every column: dx = c + bx, A = dx (ca dx)
+                // + log2 op (one rounding: the FFMA V3 compiles to), B = cb dx
+                const float ca = v1.z, cb = v1.w, lop = v3.w;
+                const uint32_t row = (uint32_t)__cvta_generic_to_shared(&s_ct[warp][lane * 17]);
+#pragma unroll
+                for (int c = 0; c < 16; c++) {
+                    const float dx = __fadd_rn((float)c, bxv);
+                    const float A1 = ((cm >> c) & 1u) ? __fmaf_rn(dx, __fmul_rn(ca, dx), lop) : -INFINITY;
+                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row + 8u * c), "f"(A1),
+                                 "f"(__fmul_rn(cb, dx)));
+                }
+                // dy pairs (dy0, dy0 + 1) of the two lane halves (rows 0 and 8)
+                const float d0 = __fadd_rn(0.f, byv), d8 = __fadd_rn(8.f, byv);
+                sts_f4(sl + 16u, make_float4(__fadd_rn(d0, 0.f), __fadd_rn(d0, 1.f), __fadd_rn(d8, 0.f),
+                                             __fadd_rn(d8, 1.f)));
+            }
         }
         __syncwarp();
         const int cnt = (int)min(32u, end - base);
@@ -291,7 +324,10 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
                 if (!need) continue;
             }
             float4 a, r3;
-            if constexpr (V3) {
+            if constexpr (CT) {
+                a = make_float4(0.f, 0.f, 0.f, 0.f);
+                r3 = make_float4(rc.w > -0.0146f ? 1.f : 0.f, 0.f, 0.f, rc.w);
+            } else if constexpr (V3) {
                 float2 cab;
                 asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(cab.x), "=f"(cab.y) : "r"(ra + 24u));
                 a = make_float4(0.f, 0.f, cab.x, cab.y);
@@ -305,9 +341,18 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
             }
             const float4 b = lds_f4(ra + 32u);  // cc, r, g, b
             const float op = r3.x;
-            const float dx = colf + rc.x;
-            const float A = a.z * dx * dx, B = a.w * dx;
-            const float dy0 = rowf + rc.y;
+            float A, B, dy0;
+            f2 dyct{0.f, 0.f};
+            if constexpr (CT) {
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(A), "=f"(B) : "r"(ct_lane + (uint32_t)q * 136u));
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(dyct.x), "=f"(dyct.y) : "r"(ra + dy_off));
+                dy0 = dyct.x;
+            } else {
+                const float dx = colf + rc.x;
+                A = a.z * dx * dx;
+                B = a.w * dx;
+                dy0 = rowf + rc.y;
+            }
             if constexpr (PACKED) {
                 // row pairs; a pixel outside the rect or at T < 1e-4 gets power
                 // -inf (alpha 0: C, T unchanged); opacities are >= 0 (clamped
@@ -317,11 +362,11 @@ __global__ void __launch_bounds__(128, MINB) composite_strip_kernel(
                 // record), so alpha = 2^pw needs no multiply and, for op <=
                 // 0.99, no 0.99 cap (alpha <= op); the reference's p = min(p,
                 // 0) only trims rounding (the conic is positive definite)
-                float A1 = TEFF ? A + __uint_as_float(__float_as_uint(r3.w)) : A;
-                if (V3 && !(mw & colbit)) A1 = -INFINITY;
+                float A1 = (TEFF && !CT) ? A + __uint_as_float(__float_as_uint(r3.w)) : A;  // CT: tabulated
+                if (V3 && !CT && !(mw & colbit)) A1 = -INFINITY;
                 const f2 A2{A1, A1}, B2{B, B}, C2{b.x, b.x}, O2{op, op}, D2{dy0, dy0};
                 const f2 R2{b.y, b.y}, G2{b.z, b.z}, Bl2{b.w, b.w}, M1{-1.f, -1.f};
-                const f2 dy01 = add2(D2, f2{0.f, 1.f});
+                const f2 dy01 = CT ? dyct : add2(D2, f2{0.f, 1.f});
                 auto pairs = [&](auto cap_c, auto full_c) {
                     constexpr bool CAP = decltype(cap_c)::value;
                     constexpr bool FULL = decltype(full_c)::value;
@@ -461,30 +506,42 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     const int ntiles = ntx * nty;
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
-    const unsigned grid = (unsigned)((warps + 3) / 4);
+    // (warps per CTA, CTAs per SM): (4, 5) = 20 warps at <= 96 registers,
+    // (4, 4) = 16 warps at <= 128, (6, 3) = 18 warps at <= 112
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char* e = getenv("GSV_COMPOSITE_CFG");
+        cfg = e ? atoi(e) : 0;
+    }
     static int packed = -1;
     if (packed < 0) {
         const char* e = getenv("GSV_COMPOSITE_PACKED");
-        packed = e ? atoi(e) : 3;
+        packed = e ? atoi(e) : 4;
     }
-#define GSV_COMPOSITE(R, P, E, V, MB)                                                                   \
+#define GSV_COMPOSITE_W(R, P, E, V, MB, W) GSV_COMPOSITE_X(R, P, E, V, MB, W, false)
+#define GSV_COMPOSITE_X(R, P, E, V, MB, W, CTB)                                                         \
     do {                                                                                                \
+        const unsigned grid = (unsigned)((warps + (W)-1) / (W));                                        \
         if (tile_off)                                                                                   \
-            composite_strip_kernel<R, P, E, true, V, MB><<<grid, 128, 0, s>>>(                          \
+            composite_strip_kernel<R, P, E, true, V, MB, W, CTB><<<grid, 32 * (W), 0, s>>>(             \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
         else                                                                                            \
-            composite_strip_kernel<R, P, E, false, V, MB><<<grid, 128, 0, s>>>(                         \
+            composite_strip_kernel<R, P, E, false, V, MB, W, CTB><<<grid, 32 * (W), 0, s>>>(            \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
     } while (0)
+#define GSV_COMPOSITE(R, P, E, V, MB) GSV_COMPOSITE_W(R, P, E, V, MB, 4)
     static int minb = -1;  // CTAs per SM the register budget is cut for (V3)
     if (minb < 0) {
         const char* e = getenv("GSV_COMPOSITE_MINB");
         minb = e ? atoi(e) : 5;
     }
-    if (packed == 3 && rows == 8) {
-        if (minb == 4) GSV_COMPOSITE(8, true, true, true, 4);
+    if (packed == 4 && rows == 8) {
+        GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);
+    } else if (packed == 3 && rows == 8) {
+        if (cfg == 2) GSV_COMPOSITE_W(8, true, true, true, 3, 6);
+        else if (minb == 4 || cfg == 1) GSV_COMPOSITE(8, true, true, true, 4);
         else GSV_COMPOSITE(8, true, true, true, 5);
     } else if (packed >= 2 && rows == 8) {
         GSV_COMPOSITE(8, true, true, false, 5);
@@ -498,6 +555,8 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
         else GSV_COMPOSITE(2, false, false, false, 5);
     }
 #undef GSV_COMPOSITE
+#undef GSV_COMPOSITE_W
+#undef GSV_COMPOSITE_X
 }
 
 }  // namespace gsv

@@ -313,8 +313,8 @@ __device__ __forceinline__ uint32_t rect_tiles(uint32_t rx, uint32_t ry) {
     return ((x1 - 1) / kTile - x0 / kTile + 1) * ((y1 - 1) / kTile - y0 / kTile + 1);
 }
 
-template <class Loader, int DEG>
-__global__ void __launch_bounds__(128, 6) project_kernel(Loader ld, CamDev cam,
+template <class Loader, int DEG, int REGS = 80>
+__global__ void __launch_bounds__(128) __maxnreg__(REGS) project_kernel(Loader ld, CamDev cam,
                                                       uint64_t* __restrict__ dkey,
                                                       uint32_t* __restrict__ didx,
                                                       SplatRec* __restrict__ rec,
@@ -409,6 +409,20 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
         project_kernel<Loader, D><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, w->rect, \
                                                             w->ctr, dbg_rect, dbg_depth);           \
     } while (0)
+    static int regs = -1;  // dev tuning: GSV_PROJ_REGS (register cap: occupancy vs spills), degree 1
+    if (regs < 0) {
+        const char* e = getenv("GSV_PROJ_REGS");
+        regs = e ? atoi(e) : 80;
+    }
+    if (sh_degree == 1 && (regs == 72 || regs == 64)) {
+        if (regs == 72)
+            project_kernel<Loader, 1, 72><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, w->rect,
+                                                                     w->ctr, dbg_rect, dbg_depth);
+        else
+            project_kernel<Loader, 1, 64><<<blocks, 128, smem, s>>>(ld, cam, w->dkey[0], w->didx[0], w->rec, w->rect,
+                                                                     w->ctr, dbg_rect, dbg_depth);
+        return;
+    }
     switch (sh_degree) {
         case 0: GSV_PROJ(0); break;
         case 1: GSV_PROJ(1); break;

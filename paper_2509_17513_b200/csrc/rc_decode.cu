@@ -42,6 +42,11 @@ __global__ void copy_planes_kernel(const CopyJob* __restrict__ jobs, int njobs) 
     for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
         const CopyJob cj = jobs[j];
         for (uint32_t i = threadIdx.x; i < cj.bytes; i += blockDim.x) cj.dst[i] = __ldg(cj.src + i);
+        // the padding up to the next word: the next plane's decoder reads its
+        // predictor a word at a time (the bytes past the plane are not used,
+        // but they are defined -- compute-sanitizer initcheck)
+        const uint32_t pad = (4u - (cj.bytes & 3u)) & 3u;
+        if (threadIdx.x < pad) cj.dst[cj.bytes + threadIdx.x] = 0;
     }
 }
 

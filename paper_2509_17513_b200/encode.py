@@ -294,7 +294,8 @@ def _gpu_finish(pending: list, codecs: Sequence[int], sess) -> list:
             caps = [int(L.gsv_encode_body_capacity(g.nf, g.chans[i][6], g.chans[i][7], g.chans[i][3]))
                     for g, i in items]
             boffs = np.concatenate([[0], np.cumsum([(c + 15) & ~15 for c in caps])]).astype(np.int64)
-            bodies = torch.empty(int(boffs[-1]) + 16, dtype=torch.uint8, device=sess.device)
+            # zeroed: the copy back below reads each body's whole capacity slot
+            bodies = torch.zeros(int(boffs[-1]) + 16, dtype=torch.uint8, device=sess.device)
             for k, (g, i) in enumerate(items):
                 _, _, _, bits, _, _, w, h = g.chans[i]
                 runs[k] = _lib.EncodeRun_t(g.planes.data_ptr() + g.offs[i], bodies.data_ptr() + int(boffs[k]),

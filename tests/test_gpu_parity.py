@@ -376,6 +376,25 @@ def test_binning_and_sort_paths_render_identically(tmp_path):
     assert np.array_equal(res["fast"], res["sort"])
 
 
+def test_compositor_variants_render_identically(tmp_path):
+    """Compositor V2 (per-lane record terms), V3 (staged quad, full-height
+    records without the vote) and V4 (the default: per-column tables) compute
+    the same operations: bit-identical images (GSV_COMPOSITE_PACKED=2/3/4)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for tag in ("2", "3", "4"):
+        f = tmp_path / f"v{tag}.npy"
+        subprocess.run([sys.executable, "-c", _PATHS_SCRIPT, root, str(f)], check=True,
+                       env={**os.environ, "GSV_COMPOSITE_PACKED": tag}, timeout=600)
+        res[tag] = np.load(f)
+    assert np.array_equal(res["2"], res["3"])
+    assert np.array_equal(res["3"], res["4"])
+
+
 @pytest.mark.parametrize("bits", [8, 16])
 def test_truncated_coded_block_is_codec_error(gsvb, bits):
     """A range-coded plane whose coded block is far shorter than the plane
