@@ -110,12 +110,14 @@ struct PlaneLoader {
     template <int DEG>
     struct Codes {
         uint32_t c[11 + SplatIn<DEG>::SHD];
+        int l;  // the splat's layer (found once, by fetch)
     };
     template <int DEG>
     __device__ __forceinline__ void fetch(uint32_t i, Codes<DEG>& k, const unsigned char* smem) const {
         const SlotDesc* s_sd = reinterpret_cast<const SlotDesc*>(smem + 256 * sizeof(double));
         int l = 0;
         while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
+        k.l = l;
         const uint32_t j = i - src.layer_off[l];
         const SlotDesc* sd = s_sd + (size_t)l * src.nslots;
 #pragma unroll
@@ -126,9 +128,7 @@ struct PlaneLoader {
                                          const unsigned char* smem) const {
         const double* s_q8 = reinterpret_cast<const double*>(smem);
         const SlotDesc* s_sd = reinterpret_cast<const SlotDesc*>(smem + 256 * sizeof(double));
-        int l = 0;
-        while (l + 1 < src.nlayers && src.layer_off[l + 1] <= i) l++;
-        const SlotDesc* sd = s_sd + (size_t)l * src.nslots;
+        const SlotDesc* sd = s_sd + (size_t)k.l * src.nslots;
 #pragma unroll
         for (int s = S0; s < S1; s++) {
             const double v = deq(k.c[s], sd[s], s_q8);
