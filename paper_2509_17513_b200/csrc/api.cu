@@ -488,8 +488,22 @@ struct gsv_video {
     // resolved by finish_open() after the stream has drained
     ErrKey stop, pending;
     std::vector<int64_t> run_order;
-    std::vector<std::string> run_name;
+    // per run (group index as decode_video names it, layer, attribute,
+    // component): the error-message prefix, formatted only when needed
+    struct RunTag {
+        int g, l, attr;
+        unsigned comp;
+    };
+    std::vector<RunTag> run_tag;
 };
+
+namespace {
+std::string run_label(const gsv_video::RunTag& t) {
+    char nm[96];
+    snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", t.g, t.l + 1, attr_name(t.attr), t.comp);
+    return nm;
+}
+}  // namespace
 
 namespace {
 
@@ -504,7 +518,7 @@ int finish_open(gsv_video* v) {
         if (v->runs.crc[r] != v->runs.runs[r].checksum) {
             const int64_t o = v->run_order[r];
             if (!best.set() || o < best.order || (o == best.order && 1 < best.phase))
-                best = {o, 1, GSV_E_CODEC, v->run_name[r] + "checksum mismatch (corrupt or truncated payload)"};
+                best = {o, 1, GSV_E_CODEC, run_label(v->run_tag[r]) + "checksum mismatch (corrupt or truncated payload)"};
             break;  // runs are in order: the first mismatch is the earliest
         }
     }
@@ -622,7 +636,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
     ErrKey& stop = v->stop;        // first structural / group-level error (walk stops there)
     ErrKey& pending = v->pending;  // first post-CRC error (plane count, valid count)
     std::vector<int64_t>& run_order = v->run_order;      // entry sequence number of each run
-    std::vector<std::string>& run_name = v->run_name;    // "group g layer l channel a[c]"
+    std::vector<gsv_video::RunTag>& run_tag = v->run_tag;  // "group g layer l channel a[c]"
     struct SlotRef { int run = -1; const Entry* e = nullptr; };
     std::vector<std::vector<std::vector<SlotRef>>> slots(G);
     int64_t seq = 0;
@@ -634,9 +648,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
             const uint32_t n_l = gd.layer_counts[l];
             for (const Entry& e : gd.channels[l]) {
                 const int64_t o = seq++;
-                char nm[96];
-                snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", gidx[g], l + 1, attr_name(e.attr),
-                         e.comp);
+                const gsv_video::RunTag tag{gidx[g], l, (int)e.attr, (unsigned)e.comp};
                 if (e.offset > len || e.size > len - e.offset) {
                     stop = {o, 0, GSV_E_FORMAT,
                             "unexpected end of container (wanted " + std::to_string(e.size) + " bytes)"};
@@ -644,17 +656,17 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                 }
                 std::string m = parse_payload(data + e.offset, e.size, true, &pr);
                 if (!m.empty()) {
-                    stop = {o, 0, GSV_E_CODEC, std::string(nm) + m};
+                    stop = {o, 0, GSV_E_CODEC, run_label(tag) + m};
                     break;
                 }
                 const int run_id = (int)v->runs.runs.size();
                 v->runs.add(pr, dev_addr(g, e.offset), (uint32_t)e.attr << 8 | e.comp);
                 run_order.push_back(o);
-                run_name.push_back(nm);
+                run_tag.push_back(tag);
                 if (pr.rd.count != gd.frame_count) {
                     if (pending.before(o, 2))
                         pending = {o, 2, GSV_E_FORMAT,
-                                   std::string(nm) + "expected " + std::to_string(gd.frame_count) +
+                                   run_label(tag) + "expected " + std::to_string(gd.frame_count) +
                                        " planes, got " + std::to_string(pr.rd.count)};
                 } else if (!(n_l > 0 && (uint64_t)n_l <= (uint64_t)pr.rd.w * pr.rd.h)) {
                     if (pending.before(o, 2)) pending = {o, 2, GSV_E_INVALID_INPUT, "valid_count out of range"};

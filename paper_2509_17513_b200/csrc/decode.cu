@@ -244,3 +244,31 @@ void launch_frame_codes(const FrameSrc& src, uint32_t* out, cudaStream_t s) {
 }
 
 }  // namespace gsv
+
+// ---------------------------------------------------------------------------
+// Dev probe (tools/e2e_probe.py): a host-to-device copy done by SMs reading
+// pinned host memory (UVA) with streaming (evict-first) stores, to measure
+// whether the copy engine's writes through L2 slow the renders beside them.
+// ---------------------------------------------------------------------------
+namespace gsv {
+__global__ void h2d_stream_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n16) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = src[i + k * stride];
+#pragma unroll
+        for (int k = 0; k < 4; k++) __stcs(dst + i + k * stride, v[k]);
+    }
+    for (; i < n16; i += stride) __stcs(dst + i, src[i]);
+}
+}  // namespace gsv
+
+extern "C" int gsv_dev_copy_h2d_stream(void* dst, const void* src, size_t n, void* stream, int blocks) {
+    const size_t n16 = n / 16;
+    if (n16)
+        gsv::h2d_stream_kernel<<<blocks > 0 ? blocks : 148, 256, 0, (cudaStream_t)stream>>>(
+            reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16);
+    return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}

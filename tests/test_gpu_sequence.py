@@ -104,3 +104,15 @@ def test_sequence_resident_device_outputs(gsvb):
         with gsvb.DeviceVideo(data, 3) as v:
             img = v.render(5, cam)
         assert torch.equal(f32[5], img)
+
+
+def test_sequence_argument_errors(gsvb):
+    from paper_2509_17513_b200.errors import InvalidInputError
+    data = container("s1_raw")
+    cam = camera("s1_raw", "axis")
+    with pytest.raises(InvalidInputError):
+        gsvb.render_sequence(data, cam, groups=[0, 7])
+    with pytest.raises(InvalidInputError):
+        gsvb.render_sequence(data, cam, up_to_layer=9)
+    with pytest.raises(InvalidInputError):  # wrong output shape
+        gsvb.render_sequence(data, cam, out=torch.empty((1, 2, 3, 3), dtype=torch.uint8))

@@ -75,8 +75,29 @@ def h2d():
     torch.cuda.synchronize()
 
 
+import ctypes
+L = _lib.load()
+L.gsv_dev_copy_h2d_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int]
+
+
+def h2dk(blocks=148):
+    L.gsv_dev_copy_h2d_stream(dcont.data_ptr(), hsrc.data_ptr(), len(data) // 16 * 16, side.cuda_stream, blocks)
+    side.synchronize()
+
+
+def h2dk32():
+    h2dk(32)
+
+
+def rend_h2dk():
+    L.gsv_dev_copy_h2d_stream(dcont.data_ptr(), hsrc.data_ptr(), len(data) // 16 * 16, side.cuda_stream, 32)
+    v.render_batch(frames, cs, outs=outs, verify=False)
+    sess.sync()
+    side.synchronize()
+
+
 for name, fn in (("seq", seq), ("rend", rend), ("rend_d2h", rend_d2h), ("rend_h2d", rend_h2d), ("d2h", d2h),
-                 ("h2d", h2d), ("seq", seq)):
+                 ("h2d", h2d), ("h2dk", h2dk), ("h2dk32", h2dk32), ("rend_h2dk", rend_h2dk), ("seq", seq)):
     fn()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
