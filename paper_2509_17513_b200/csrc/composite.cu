@@ -155,8 +155,11 @@ __device__ __forceinline__ float ex2f(float x) {
 // loads: (A, B) of its column, its half's dy pair, (cc, r, g, b), and the
 // mask / log2-op pair.  The arithmetic is V3's, op for op (bit-identical).
 // The table rows are 17 float2 apart (bank-conflict-free both ways).
+//
+// FLAG0: every strip reads the tile's state from strip 0's flag byte (a last
+// round split finer than round 1, whose ROWS = 8 warps set only strip 0).
 template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5, int WPC = 4,
-          bool CT = false>
+          bool CT = false, bool FLAG0 = false>
 __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >= 5 ? 96 : 128)) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
     if (tile >= ntiles) return;
     // per-strip state: saturated strips were written out in an earlier round;
     // blank ones too, unless this round brings their tile keys
-    uint8_t* flag = tile_done + 4 * (size_t)tile + strip;
+    uint8_t* flag = tile_done + 4 * (size_t)tile + (FLAG0 ? 0 : strip);
     const uint8_t td = first ? kTileOpen : *flag;
     if (td == kTileSaturated) return;
     const uint32_t K = (uint32_t)*nkeys;
@@ -536,6 +539,27 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     if (minb < 0) {
         const char* e = getenv("GSV_COMPOSITE_MINB");
         minb = e ? atoi(e) : 5;
+    }
+    static int r2rows = -1;  // rows per lane of a last round after a first one (GSV_R2_ROWS: 8, 4 or 2)
+    if (r2rows < 0) {
+        const char* e = getenv("GSV_R2_ROWS");
+        r2rows = e ? atoi(e) : 8;
+        if (r2rows != 2 && r2rows != 4) r2rows = 8;
+    }
+    if (!first && last && rows == 8 && r2rows != 8 && tile_off) {
+        // the few tiles still open after round 1 walk long record lists one
+        // warp each; 2 (ROWS = 4) or 4 (ROWS = 2) warps per tile shorten that
+        // latency-bound walk
+        const unsigned g4 = (unsigned)((ntiles * (16 / (2 * r2rows)) + 3) / 4);
+        if (r2rows == 4)
+            composite_strip_kernel<4, true, false, true, false, 5, 4, false, true><<<g4, 128, 0, s>>>(
+                keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first,
+                last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);
+        else
+            composite_strip_kernel<2, true, false, true, false, 5, 4, false, true><<<g4, 128, 0, s>>>(
+                keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first,
+                last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);
+        return;
     }
     if (packed == 4 && rows == 8) {
         GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);

@@ -253,7 +253,7 @@ def _gpu_quantize_group(frames: list, start: int, cfg: EncodeConfig, position_bi
         cols = torch.empty((ncol, nf, n), dtype=torch.float64, device=dev)  # significance order
         for t, f in enumerate(frames):
             for c0, a in ((0, f.positions), (3, f.rotations), (7, f.scales), (10, f.opacities), (11, f.sh)):
-                a = torch.from_numpy(np.ascontiguousarray(a, np.float64).reshape(len(f), -1)).to(dev)
+                a = torch.from_numpy(np.require(a, np.float64, ["C", "W"]).reshape(len(f), -1)).to(dev)
                 cols[c0:c0 + a.shape[1], t, :] = a.index_select(0, d_idx).t()
         rot = cols[3:7]
         for t in range(1, nf):

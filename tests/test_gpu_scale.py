@@ -18,6 +18,8 @@ BASELINE geometry:
 * config 5 geometry: 1M splats at 3840x2160 (32,400 tiles: round-1 binning)
   and at 4096x2304 (36,864 tiles: above the binning limit, emit + sort);
 * config 4: two of the 16 ring cameras at 500k splats;
+* config 3: 1M splats in 2-frame adaptive groups, both codecs (codes of a
+  range-coded group, projection, image, render_sequence's frames);
 * depth-order robustness: a near-planar scene and one whose depth range is
   stretched by a far outlier (long runs of equal truncated sort keys).
 
@@ -193,6 +195,48 @@ def test_c4_ring_cameras(gsvb):
         for view in (3, 10):
             proj = check_projection(v, 0, cams[view], osets[0])
             check_image(v, 0, cams[view], proj)
+
+
+def test_c3_short_groups_1m(gsvb):
+    """Config 3 shape: 1M Gaussians, 6 layers, a burst every 2 frames (the
+    2-frame adaptive groups), 6 frames = 3 groups, both codecs.  The codes of
+    every frame of group 1 (its range-coded second plane under the model the
+    keyframe plane trained) equal the oracle's; frame 3 projects bit-exactly
+    and renders within tolerance; render_sequence's u8 frames equal the
+    per-frame renders for both codecs."""
+    import torch
+    from paper_2509_17513_b200.configs import CONFIGS
+    cfg = CONFIGS["c3"]
+    blobs, _ = _encode(cfg, 6)
+    info = gsvb.read_structure(blobs[1])
+    assert len(info.groups) >= 3 and info.groups[1].start_frame == 2 and info.groups[1].frame_count == 2
+    for codec in (0, 1):
+        data = blobs[codec]
+        info_o = O.read_structure(data)
+        vals = O.decode_group_codes(data, info_o, 1, cfg.layers)
+        order = [("position", c) for c in range(3)] + [("rotation", c) for c in range(4)] + \
+            [("scales", c) for c in range(3)] + [("opacity", 0)] + \
+            [("sh", c) for c in range(3 * (info_o.sh_degree + 1) ** 2)]
+        with gsvb.DeviceVideo(data, cfg.layers) as v:
+            assert v.splat_count(2) == 1_000_000
+            for t in (2, 3):  # group 1
+                got = v.frame_codes(t).cpu().numpy().astype(np.uint32)
+                exp = np.concatenate([np.stack([vals[l][key][0][t - 2] for key in order], axis=1)
+                                      for l in range(cfg.layers)])
+                assert np.array_equal(got, exp), (codec, t)
+            sets = O.assemble(info_o, info_o.groups[1], vals, cfg.layers, only=[1])
+            cam = cfg.cameras()[0]
+            proj = check_projection(v, 3, cam, sets[0])
+            check_image(v, 3, cam, proj)
+        import dataclasses
+        small = dataclasses.replace(cam, fx=cam.fx / 4, fy=cam.fy / 4, cx=cam.cx / 4, cy=cam.cy / 4,
+                                    width=cam.width // 4, height=cam.height // 4)
+        seq = gsvb.render_sequence(data, small)
+        with gsvb.DeviceVideo(data, cfg.layers) as v:
+            for t in range(6):
+                u8 = torch.empty((small.height, small.width, 3), dtype=torch.uint8, device="cuda")
+                v.render(t, small, out_u8=u8)
+                assert torch.equal(seq[t], u8.cpu()), (codec, t)
 
 
 @pytest.mark.parametrize("size", [(3840, 2160), (4096, 2304)], ids=["4k_binned", "above_32768_tiles"])

@@ -63,8 +63,12 @@ def seq_e2e():
     g.render_sequence(hsrc, cs, up_to_layer=6, out=pinned, session=sess, info=info)
 
 
+def seq_res():
+    g.render_sequence(data, cs, up_to_layer=6, resident=res, outs=outs, session=sess, info=info)
+
+
 for name, fn in (("full", full), ("open", open_only), ("render", render_only), ("render30", render30),
-                 ("seq_e2e", seq_e2e), ("full", full)):
+                 ("seq_e2e", seq_e2e), ("seq_res", seq_res), ("full", full), ("seq_res", seq_res)):
     for _ in range(2):
         fn()
     torch.cuda.synchronize()
