@@ -60,6 +60,7 @@ struct gsv_session {
     // synchronise, so they are not taken from the pool on every call)
     std::vector<uint8_t*> seq_slot;
     std::vector<size_t> seq_slot_cap;
+    std::vector<cudaEvent_t> ev_plane;  // first group uploaded plane-major: frame f's planes landed
 };
 
 namespace {
@@ -822,6 +823,7 @@ void gsv_session_destroy(gsv_session* s) {
     }
     if (s->ev_prep) cudaEventDestroy(s->ev_prep);
     for (cudaEvent_t e : s->ev_up) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->ev_plane) cudaEventDestroy(e);
     for (uint8_t* p : s->seq_slot)
         if (p) cudaFree(p);
     for (cudaEvent_t e : s->ev_slot_done) cudaEventDestroy(e);
@@ -990,12 +992,13 @@ int ensure_aux(gsv_session* s, int nstreams, size_t img8, bool host_out) {
 // Nothing is joined back into the session stream.
 int enqueue_frames(gsv_video* v, const int32_t* frames, int count, const CamDev& cd, size_t img8,
                    float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8, int nstreams,
-                   int first) {
+                   int first, const cudaEvent_t* frame_ready = nullptr) {
     gsv_session* s = v->s;
     GSV_CUDA(cudaEventRecord(s->ev_fork, s->stream));
     for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaStreamWaitEvent(s->aux[i], s->ev_fork, 0));
     for (int j = 0; j < count; j++) {
         const int i = (first + j) % nstreams;
+        if (frame_ready) GSV_CUDA(cudaStreamWaitEvent(s->aux[i], frame_ready[j], 0));  // its planes landed
         FrameSrc src;
         int rc = frame_src(v, frames[j], &src);
         if (rc) return rc;
@@ -1095,6 +1098,47 @@ struct VideoList {
         for (gsv_video* x : v) delete x;
     }
 };
+
+// Plane-major upload of a raw group: its runs of one sample width in one
+// layer follow each other with a constant stride in the container (header,
+// count x plane, CRC), so plane f of all of them is one 2-D copy.  Returns
+// the copies grouped by plane (empty when the layout is not regular).
+struct PlaneCopy {
+    uint64_t src_off;  // container offset of plane f of the first run
+    uint64_t pitch, width, height;
+};
+std::vector<std::vector<PlaneCopy>> plane_major_plan(const uint8_t* data, const GroupDir& gd, int k) {
+    const int F = gd.frame_count;
+    std::vector<std::vector<PlaneCopy>> plan(F);
+    for (int l = 0; l < k; l++) {
+        const auto& ents = gd.channels[l];
+        size_t i = 0;
+        while (i < ents.size()) {
+            const uint8_t* b = data + ents[i].offset;
+            const uint64_t hdr = b[0] == 0 ? 14 : 15;  // codec 0 body / codec 1 raw-fallback body
+            const uint64_t pb = (uint64_t)rd16(b + 2) * rd16(b + 4) * (b[1] / 8);
+            // the longest run of entries with the same layout at a constant stride
+            size_t j = i + 1;
+            uint64_t stride = 0;
+            while (j < ents.size()) {
+                const uint8_t* c = data + ents[j].offset;
+                const uint64_t hj = c[0] == 0 ? 14 : 15;
+                const uint64_t pj = (uint64_t)rd16(c + 2) * rd16(c + 4) * (c[1] / 8);
+                const uint64_t st = ents[j].offset - ents[j - 1].offset;
+                if (hj != hdr || pj != pb || (j > i + 1 && st != stride) || ents[j].offset < ents[j - 1].offset)
+                    break;
+                stride = st;
+                j++;
+            }
+            if (j == i + 1) stride = pb;  // a single run: the pitch is irrelevant
+            if (stride < pb) return {};
+            for (int f = 0; f < F; f++)
+                plan[f].push_back(PlaneCopy{ents[i].offset + hdr + (uint64_t)f * pb, stride, pb, (uint64_t)(j - i)});
+            i = j;
+        }
+    }
+    return plan;
+}
 
 bool group_is_raw(const uint8_t* data, size_t len, const GroupDir& gd, int k) {
     for (int l = 0; l < k; l++)
@@ -1249,14 +1293,40 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
         mark("start", -1, s->stream);
         int err = GSV_OK;
         int64_t fo = 0;
+        // GSV_SEQ_PLANE_MAJOR=1: the first group goes up plane-major (plane f
+        // of every run, then f + 1, ...: 2-D copies over the runs' constant
+        // stride) so that its frame f can render as soon as its planes have
+        // landed.  Off: the copy engine moves the 2-D copies at ~24 GB/s
+        // against 55 for one contiguous copy, which delays every later group
+        // (measured 76 vs 73 ms per config-2 step)
+        static const bool pm_env = getenv("GSV_SEQ_PLANE_MAJOR") && atoi(getenv("GSV_SEQ_PLANE_MAJOR")) != 0;
+        std::vector<std::vector<PlaneCopy>> pm0;
+        if (pm_env && !resident) pm0 = plane_major_plan(data, c.groups[sel[0]], k);
+        const bool plane_major = !pm0.empty();
+        if (plane_major)
+            while (s->ev_plane.size() < pm0.size()) {
+                cudaEvent_t e;
+                GSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                s->ev_plane.push_back(e);
+            }
         auto upload_group = [&](int gi) -> int {
             const int r = gi % R;
             if (gi >= R)  // ring: the slot's previous group has rendered
                 for (int i = 0; i < nstreams; i++)
                     GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + i], 0));
             if (gi >= R) GSV_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_slot_done[(r % kSeqSlots) * 33 + 32], 0));
-            GSV_CUDA(cudaMemcpyAsync(slot[r], data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
-                                     s->copy_in));
+            if (gi == 0 && plane_major) {
+                for (size_t f = 0; f < pm0.size(); f++) {
+                    for (const PlaneCopy& pc : pm0[f])
+                        GSV_CUDA(cudaMemcpy2DAsync(slot[r] + (pc.src_off - lo[0]), pc.pitch, data + pc.src_off,
+                                                   pc.pitch, pc.width, pc.height, cudaMemcpyHostToDevice,
+                                                   s->copy_in));
+                    GSV_CUDA(cudaEventRecord(s->ev_plane[f], s->copy_in));
+                }
+            } else {
+                GSV_CUDA(cudaMemcpyAsync(slot[r], data + lo[gi], hi[gi] - lo[gi], cudaMemcpyHostToDevice,
+                                         s->copy_in));
+            }
             GSV_CUDA(cudaEventRecord(s->ev_up[r], s->copy_in));
             mark("uploaded", gi, s->copy_in);
             return GSV_OK;
@@ -1301,7 +1371,8 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
             }
             gsv_video* v = vids.v[gi];
             if (!all_slots && (err = upload_group(gi))) break;
-            if (!resident) GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
+            // (the plane-major first group: its frames wait for their own planes)
+            if (!resident && !(gi == 0 && plane_major)) GSV_CUDA(cudaStreamWaitEvent(s->stream, s->ev_up[r], 0));
             // renders fork before the group's CRC (validation only): they never
             // wait for the CRC kernel, which runs as SM resources free up
             v->runs.launch_planes(s->stream);
@@ -1310,7 +1381,7 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
             for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
             err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, out_rgb ? out_rgb + fo : nullptr,
                                  out_rgb8 ? out_rgb8 + fo : nullptr, host_rgb8 ? host_rgb8 + fo : nullptr, nstreams,
-                                 (int)(fo % nstreams));
+                                 (int)(fo % nstreams), (gi == 0 && plane_major) ? s->ev_plane.data() : nullptr);
             if (err) break;
             for (int i = 0; i < nstreams && dbg; i++) mark("rendered", gi, s->aux[i]);
             for (int i = 0; i < nstreams && dbg && host_out; i++) mark("copied", gi, s->aux_copy[i]);
