@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(128) __maxnreg__(REGS) project_kernel(Loader l
     extern __shared__ __align__(16) unsigned char proj_smem[];
     ld.stage(proj_smem);
     const int64_t n = ld.count();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // persistent CTAs (grid <= one wave): the slot descriptors and quotient
+    // table are staged once per CTA, not once per 128 splats
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
     bool alive = false;
     uint64_t key = ~0ull;
     uint32_t ntile = 0;  // (tile, splat) overlaps of this splat's rect (render stats)
@@ -393,14 +396,25 @@ __global__ void __launch_bounds__(128) __maxnreg__(REGS) project_kernel(Loader l
         atomicMax(ctr + 3, (unsigned long long)kmax);
         atomicAdd(ctr + 10, tot);  // C_TOTK
     }
+    }
 }
 
 template <class Loader>
 void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degree, RenderWork* w,
                     int32_t* dbg_rect, double* dbg_depth, cudaStream_t s) {
     if (n <= 0) return;
-    const unsigned blocks = (unsigned)((n + 127) / 128);
     const size_t smem = Loader::smem_bytes(ld.src);
+    static int wave = -1;  // CTAs of one wave on this device (persistent grid)
+    if (wave < 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* e = getenv("GSV_PROJ_WAVES");  // dev: waves of CTAs (0: one CTA per 128 splats)
+        const int waves = e ? atoi(e) : 1;
+        wave = waves > 0 ? sms * 6 * waves : 0;
+    }
+    unsigned blocks = (unsigned)((n + 127) / 128);
+    if (wave > 0 && blocks > (unsigned)wave) blocks = (unsigned)wave;
 #define GSV_PROJ(D)                                                                                 \
     do {                                                                                            \
         if (smem > 48 * 1024)                                                                       \
