@@ -179,7 +179,8 @@ int gsv_session_check_capacity(gsv_session* s);
  * frame), pipelined in one call -- group uploads, opens and renders with
  * read-back overlap; CRC and structural errors are reported as decode_video
  * raises them (first in decode order), after the pipeline has drained.
- * frames_out (may be NULL): frames written. */
+ * frames_out (may be NULL): frames written.  The session keeps the device
+ * payload slots (the container's layer-prefix bytes) for its next call. */
 int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, int up_to_layer,
                              const int32_t* groups, int ngroups, const gsv_camera* cam,
                              uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out);

@@ -1176,10 +1176,13 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
     if (groups && ngroups > 0) sel.assign(groups, groups + ngroups);
     else
         for (int g = 0; g < (int)c.groups.size(); g++) sel.push_back(g);
-    for (int g : sel)
+    std::vector<char> seen(c.groups.size(), 0);
+    for (int g : sel) {
         if (g < 0 || g >= (int)c.groups.size())
             return fail(GSV_E_INVALID_INPUT, "group " + std::to_string(g) + " out of range 0.." +
                                                  std::to_string((int)c.groups.size() - 1));
+        if (seen[g]++) return fail(GSV_E_INVALID_INPUT, "group " + std::to_string(g) + " listed twice");
+    }
     const int L = c.layer_count;
     const int k = up_to_layer == -1 ? L : up_to_layer;
     if (k < 1 || k > L)

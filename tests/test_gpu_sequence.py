@@ -114,5 +114,7 @@ def test_sequence_argument_errors(gsvb):
         gsvb.render_sequence(data, cam, groups=[0, 7])
     with pytest.raises(InvalidInputError):
         gsvb.render_sequence(data, cam, up_to_layer=9)
+    with pytest.raises(InvalidInputError):  # a group listed twice
+        gsvb.render_sequence(data, cam, groups=[0, 0])
     with pytest.raises(InvalidInputError):  # wrong output shape
         gsvb.render_sequence(data, cam, out=torch.empty((1, 2, 3, 3), dtype=torch.uint8))
