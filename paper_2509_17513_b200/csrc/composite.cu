@@ -158,8 +158,11 @@ __device__ __forceinline__ float ex2f(float x) {
 //
 // FLAG0: every strip reads the tile's state from strip 0's flag byte (a last
 // round split finer than round 1, whose ROWS = 8 warps set only strip 0).
+//
+// DYT (V5, with CT): the table row also holds both lane halves' four
+// (dy, dy + 1) pairs (rows 208 B apart), so no lane adds the row offsets.
 template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5, int WPC = 4,
-          bool CT = false, bool FLAG0 = false>
+          bool CT = false, bool FLAG0 = false, bool DYT = false>
 __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >= 5 ? 96 : 128)) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
@@ -168,7 +171,8 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
     uint8_t* __restrict__ out_rgb8) {
     constexpr int kStrips = 16 / (2 * ROWS);  // warps per tile, each fully independent
     __shared__ __align__(16) float4 s_rec[2][WPC][32 * 4];  // double-buffered per-warp batches
-    __shared__ __align__(16) float2 s_ct[CT ? WPC : 1][CT ? 32 * 17 : 1];  // V4 column tables
+    constexpr int kRow = DYT ? 26 : 17;  // float2 per table row
+    __shared__ __align__(16) float2 s_ct[CT ? WPC : 1][CT ? 32 * kRow : 1];  // V4 column tables
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw = blockIdx.x * WPC + warp;
     const int tile = gw / kStrips, strip = gw % kStrips;
@@ -206,6 +210,8 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
     // offset of its half's dy pair in a staged record
     const uint32_t ct_lane = CT ? (uint32_t)__cvta_generic_to_shared(&s_ct[warp][0]) + 8u * colsh : 0u;
     const uint32_t dy_off = 16u + 8u * (uint32_t)(lane >> 4);
+    const uint32_t ct_row0 = CT ? (uint32_t)__cvta_generic_to_shared(&s_ct[warp][0]) + 128u + 32u * (uint32_t)(lane >> 4)
+                                : 0u;
     float T[ROWS], c0[ROWS], c1[ROWS], c2[ROWS];
     uint32_t live = 0, inimg = 0;
     const bool work = on && start < end;
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
                 // the per-lane V3 terms, for every column: dx = c + bx, A = dx (ca dx)
                 // + log2 op (one rounding: the FFMA V3 compiles to), B = cb dx
                 const float ca = v1.z, cb = v1.w, lop = v3.w;
-                const uint32_t row = (uint32_t)__cvta_generic_to_shared(&s_ct[warp][lane * 17]);
+                const uint32_t row = (uint32_t)__cvta_generic_to_shared(&s_ct[warp][lane * kRow]);
 #pragma unroll
                 for (int c = 0; c < 16; c++) {
                     const float dx = __fadd_rn((float)c, bxv);
@@ -296,6 +302,15 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
                 const float d0 = __fadd_rn(0.f, byv), d8 = __fadd_rn(8.f, byv);
                 sts_f4(sl + 16u, make_float4(__fadd_rn(d0, 0.f), __fadd_rn(d0, 1.f), __fadd_rn(d8, 0.f),
                                              __fadd_rn(d8, 1.f)));
+                if constexpr (DYT) {  // pair j of half h: ((d + 0) + j, (d + 1) + j), as V3 adds it
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const float d = h ? d8 : d0, e0 = __fadd_rn(d, 0.f), e1 = __fadd_rn(d, 1.f);
+                        sts_f4(row + 128u + 32u * h, make_float4(e0, e1, __fadd_rn(e0, 2.f), __fadd_rn(e1, 2.f)));
+                        sts_f4(row + 144u + 32u * h,
+                               make_float4(__fadd_rn(e0, 4.f), __fadd_rn(e1, 4.f), __fadd_rn(e0, 6.f), __fadd_rn(e1, 6.f)));
+                    }
+                }
             }
         }
         __syncwarp();
@@ -346,10 +361,20 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
             const float op = r3.x;
             float A, B, dy0;
             f2 dyct{0.f, 0.f};
+            f2 dyt[4];  // DYT: this lane half's four row-pair dy values
             if constexpr (CT) {
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(A), "=f"(B) : "r"(ct_lane + (uint32_t)q * 136u));
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(A), "=f"(B)
+                             : "r"(ct_lane + (uint32_t)q * (8u * kRow)));
                 asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(dyct.x), "=f"(dyct.y) : "r"(ra + dy_off));
                 dy0 = dyct.x;
+                if constexpr (DYT) {
+                    const uint32_t dyrow = ct_row0 + (uint32_t)q * (8u * kRow);
+                    const float4 p01 = lds_f4(dyrow), p23 = lds_f4(dyrow + 16u);
+                    dyt[0] = f2{p01.x, p01.y};
+                    dyt[1] = f2{p01.z, p01.w};
+                    dyt[2] = f2{p23.x, p23.y};
+                    dyt[3] = f2{p23.z, p23.w};
+                }
             } else {
                 const float dx = colf + rc.x;
                 A = a.z * dx * dx;
@@ -382,7 +407,7 @@ __global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >
                         // with weight 0
                         if (!FULL && !(need & (3u << j))) continue;
                         // (j, j) broadcast: an immediate operand, no pair constant to build
-                        const f2 dy = j ? add2(dy01, f2{(float)j, (float)j}) : dy01;
+                        const f2 dy = DYT ? dyt[j / 2] : (j ? add2(dy01, f2{(float)j, (float)j}) : dy01);
                         f2 pw = fma2(fma2(C2, dy, B2), dy, A2);
                         f2 te, al;
                         if (FULL) {
@@ -522,15 +547,16 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
         packed = e ? atoi(e) : 4;
     }
 #define GSV_COMPOSITE_W(R, P, E, V, MB, W) GSV_COMPOSITE_X(R, P, E, V, MB, W, false)
-#define GSV_COMPOSITE_X(R, P, E, V, MB, W, CTB)                                                         \
+#define GSV_COMPOSITE_X(R, P, E, V, MB, W, CTB) GSV_COMPOSITE_Y(R, P, E, V, MB, W, CTB, false)
+#define GSV_COMPOSITE_Y(R, P, E, V, MB, W, CTB, DY)                                                     \
     do {                                                                                                \
         const unsigned grid = (unsigned)((warps + (W)-1) / (W));                                        \
         if (tile_off)                                                                                   \
-            composite_strip_kernel<R, P, E, true, V, MB, W, CTB><<<grid, 32 * (W), 0, s>>>(             \
+            composite_strip_kernel<R, P, E, true, V, MB, W, CTB, false, DY><<<grid, 32 * (W), 0, s>>>(  \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
         else                                                                                            \
-            composite_strip_kernel<R, P, E, false, V, MB, W, CTB><<<grid, 32 * (W), 0, s>>>(            \
+            composite_strip_kernel<R, P, E, false, V, MB, W, CTB, false, DY><<<grid, 32 * (W), 0, s>>>( \
                 keys, tile_off, ranks, nkeys, recs, state, tile_done, cam.width, cam.height, ntx, ntiles, first, \
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);                              \
     } while (0)
@@ -561,7 +587,9 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
                 last, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_rgb8);
         return;
     }
-    if (packed == 4 && rows == 8) {
+    if (packed == 5 && rows == 8) {
+        GSV_COMPOSITE_Y(8, true, true, true, 5, 4, true, true);
+    } else if (packed == 4 && rows == 8) {
         GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);
     } else if (packed == 3 && rows == 8) {
         if (cfg == 2) GSV_COMPOSITE_W(8, true, true, true, 3, 6);
@@ -581,6 +609,7 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
 #undef GSV_COMPOSITE
 #undef GSV_COMPOSITE_W
 #undef GSV_COMPOSITE_X
+#undef GSV_COMPOSITE_Y
 }
 
 }  // namespace gsv
