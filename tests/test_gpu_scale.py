@@ -15,7 +15,7 @@ BASELINE geometry:
   equal to write_ppm's rounding;
 * config 2 codec 1: the decoded integer codes of frames 1, 15 and 29 of the
   30-frame group (model persistence across 29 planes) against the oracle;
-* config 5 geometry: 1M splats at 3840x2160 (32,400 tiles: round-1 binning)
+* config 5: a 3M-splat 4K frame; and 1M splats at 3840x2160 (32,400 tiles: round-1 binning)
   and at 4096x2304 (36,864 tiles: above the binning limit, emit + sort);
 * config 4: two of the 16 ring cameras at 500k splats;
 * config 3: 1M splats in 2-frame adaptive groups, both codecs (codes of a
@@ -237,6 +237,22 @@ def test_c3_short_groups_1m(gsvb):
                 u8 = torch.empty((small.height, small.width, 3), dtype=torch.uint8, device="cuda")
                 v.render(t, small, out_u8=u8)
                 assert torch.equal(seq[t], u8.cpu()), (codec, t)
+
+
+def test_c5_full_scale_frame(gsvb):
+    """Config 5 at its own scale: 3M Gaussians (config 5's recipe), 6 layers,
+    one frame at 3840x2160 -- projection, stable order and tile counts
+    bit-exact against the oracle, image within 2e-3, u8 = write_ppm."""
+    from paper_2509_17513_b200.configs import CONFIGS
+    cfg = CONFIGS["c5"]
+    blobs, _ = _encode(cfg, 1, codecs=(0,))
+    data = blobs[0]
+    cam = cfg.cameras()[0]
+    _, _, osets = _oracle_frames(data, cfg.layers, [0])
+    with gsvb.DeviceVideo(data, cfg.layers) as v:
+        assert v.splat_count(0) == 3_000_000
+        proj = check_projection(v, 0, cam, osets[0])
+        check_image(v, 0, cam, proj)
 
 
 @pytest.mark.parametrize("size", [(3840, 2160), (4096, 2304)], ids=["4k_binned", "above_32768_tiles"])
