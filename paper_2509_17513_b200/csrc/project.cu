@@ -409,8 +409,13 @@ void launch_project(const Loader& ld, int64_t n, const CamDev& cam, int sh_degre
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char* e = getenv("GSV_PROJ_WAVES");  // dev: waves of CTAs (0: one CTA per 128 splats)
-        const int waves = e ? atoi(e) : 1;
+        // dev: GSV_PROJ_WAVES=k caps the grid at k waves of persistent CTAs
+        // (descriptors staged once per CTA).  Default 0, one CTA per 128
+        // splats: equal throughput in the frame-parallel mix, but a lone
+        // projection runs 62 us persistent vs 41 us (no overlap between a
+        // CTA's iterations)
+        const char* e = getenv("GSV_PROJ_WAVES");
+        const int waves = e ? atoi(e) : 0;
         wave = waves > 0 ? sms * 6 * waves : 0;
     }
     unsigned blocks = (unsigned)((n + 127) / 128);
