@@ -1227,10 +1227,15 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
     // of kSeqSlots slots, each reused once its group has rendered.
     uint64_t total = 0;
     for (int gi = 0; gi < G; gi++) total += ((hi[gi] - lo[gi]) + 255) & ~255ull;
+    // free HBM: queried only when the slots the session already holds are
+    // too small (cudaMemGetInfo can take milliseconds while copies run)
+    uint64_t held = 0;
+    for (size_t r = 0; r < s->seq_slot_cap.size() && r < (size_t)G; r++) held += s->seq_slot_cap[r];
     size_t mfree = 0, mtot = 0;
-    cudaMemGetInfo(&mfree, &mtot);
+    if (!resident && held < total) cudaMemGetInfo(&mfree, &mtot);
     const char* ring_env = getenv("GSV_SEQ_RING");  // tests: force the ring of slots
-    const bool all_slots = resident || (total <= mfree / 4 && !(ring_env && atoi(ring_env) != 0));
+    const bool fits = held >= total || total <= (held + mfree) / 4;
+    const bool all_slots = resident || (fits && !(ring_env && atoi(ring_env) != 0));
     const int R = all_slots ? G : std::min(kSeqSlots, G);
     if (!s->copy_in) GSV_CUDA(cudaStreamCreateWithFlags(&s->copy_in, cudaStreamNonBlocking));
     if (!s->check) GSV_CUDA(cudaStreamCreateWithFlags(&s->check, cudaStreamNonBlocking));
@@ -1269,7 +1274,9 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
     auto dev_base = [&](int gi) -> const uint8_t* { return resident ? dev_data : slot[gi % R] - lo[gi]; };
     // the pinned staging of the deferred opens is reset once, with the
     // session stream drained (nothing of an earlier call still reads it)
+    const auto t_sync = std::chrono::steady_clock::now();
     GSV_CUDA(cudaStreamSynchronize(s->stream));
+    const auto t_reset = std::chrono::steady_clock::now();
     t_stage.reset();
     // dev: GSV_DEBUG_SEQ_TIMING=1 prints a per-group timeline (CUDA events)
     static const bool dbg = getenv("GSV_DEBUG_SEQ_TIMING") != nullptr;
@@ -1281,8 +1288,12 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
     };
     std::vector<Mark> marks;
     const auto h0 = std::chrono::steady_clock::now();
-    if (dbg) fprintf(stderr, "[seq] host: setup (parse, slots, sync) %.3f ms\n",
-                     std::chrono::duration<double, std::milli>(h0 - t_entry).count());
+    if (dbg)
+        fprintf(stderr, "[seq] host: setup (parse, slots, sync) %.3f ms (to sync %.3f, sync %.3f, stage reset %.3f)\n",
+                std::chrono::duration<double, std::milli>(h0 - t_entry).count(),
+                std::chrono::duration<double, std::milli>(t_sync - t_entry).count(),
+                std::chrono::duration<double, std::milli>(t_reset - t_sync).count(),
+                std::chrono::duration<double, std::milli>(h0 - t_reset).count());
     auto mark = [&](const char* what, int g, cudaStream_t st) {
         if (!dbg) return;
         cudaEvent_t e;

@@ -25,7 +25,7 @@ cs = _lib.camera_struct(bench.camera(A))
 sess = g.Session(0)
 hsrc = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
 pinned = torch.empty((300, 1080, 1920, 3), dtype=torch.uint8).pin_memory()
-for i in range(6):
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     t0 = time.perf_counter()
     g.render_sequence(hsrc, cs, up_to_layer=6, out=pinned, session=sess, info=info)
     print(f"call {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms", file=sys.stderr, flush=True)
