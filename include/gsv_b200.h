@@ -139,6 +139,10 @@ int gsv_video_open_groups(gsv_session* s, const uint8_t* data, size_t len, int u
  * in range and distinct. */
 int gsv_video_open_group_list(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
                               int up_to_layer, const int32_t* groups, int ngroups, gsv_video** out);
+/* Does not wait: the video's device memory is released once the work
+ * enqueued on its session so far has completed (reaped by later opens and
+ * closes, or gsv_session_destroy).  Host outputs of earlier render_batch
+ * calls are complete after gsv_session_sync. */
 void gsv_video_close(gsv_video* v);
 int gsv_video_frame_count(const gsv_video* v);
 int gsv_video_decoded_layers(const gsv_video* v);

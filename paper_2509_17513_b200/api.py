@@ -405,7 +405,9 @@ class DeviceVideo:
                      streams: int = 8, verify: bool = True):
         """Render frames[j] frame-parallel on `streams` CUDA streams.  outs /
         outs_u8: per-frame device tensors (fp32 / u8, (H, W, 3)) or None;
-        host_u8: per-frame host (pinned) u8 tensors filled by D2H copies."""
+        host_u8: per-frame host (pinned) u8 tensors filled by D2H copies
+        (complete once the session is synchronised: Session.sync or
+        torch.cuda.synchronize)."""
         n = len(frames)
         c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
         fr = (ctypes.c_int32 * n)(*[int(t) for t in frames])

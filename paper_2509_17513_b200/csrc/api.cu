@@ -61,6 +61,11 @@ struct gsv_session {
     std::vector<uint8_t*> seq_slot;
     std::vector<size_t> seq_slot_cap;
     std::vector<cudaEvent_t> ev_plane;  // first group uploaded plane-major: frame f's planes landed
+    // closed videos whose buffers may still be read by enqueued work: freed
+    // once the event recorded at close has completed (gsv_video_close does
+    // not synchronise, so the next open's host work overlaps the GPU tail)
+    std::vector<std::pair<cudaEvent_t, gsv_video*>> graveyard;
+    std::vector<cudaEvent_t> free_events;
 };
 
 namespace {
@@ -499,6 +504,22 @@ struct gsv_video {
 };
 
 namespace {
+// free the closed videos whose work has completed (or all, waiting, if wait)
+void reap_closed(gsv_session* s, bool wait) {
+    size_t keep = 0;
+    for (size_t i = 0; i < s->graveyard.size(); i++) {
+        auto& g = s->graveyard[i];
+        if (wait) cudaEventSynchronize(g.first);
+        if (wait || cudaEventQuery(g.first) == cudaSuccess) {
+            delete g.second;
+            s->free_events.push_back(g.first);
+        } else {
+            s->graveyard[keep++] = g;
+        }
+    }
+    s->graveyard.resize(keep);
+    cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+}
 std::string run_label(const gsv_video::RunTag& t) {
     char nm[96];
     snprintf(nm, sizeof nm, "group %d layer %d channel %s[%u]: ", t.g, t.l + 1, attr_name(t.attr), t.comp);
@@ -540,6 +561,7 @@ int open_video(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* d
                int up_to_layer, gsv_video** out, const std::vector<int>* sel = nullptr, bool deferred = false,
                bool prepare_only = false) {
     if (prepare_only) deferred = true;
+    reap_closed(s, false);
     *out = nullptr;
     if (!deferred) t_stage.reset();
     static const bool dbg_t = getenv("GSV_DEBUG_OPEN_TIMING") != nullptr;  // dev: phase times to stderr
@@ -797,6 +819,8 @@ void gsv_session_destroy(gsv_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
+    reap_closed(s, true);
+    for (cudaEvent_t e : s->free_events) cudaEventDestroy(e);
     for (size_t i = 0; i < s->aux.size(); i++) {
         cudaStreamSynchronize(s->aux[i]);
         cudaStreamSynchronize(s->aux_copy[i]);
@@ -883,10 +907,26 @@ int gsv_video_open_group_list(gsv_session* s, const uint8_t* data, size_t len, c
     return open_video(s, data, len, dev_data, up_to_layer, out, &sel);
 }
 
+
 void gsv_video_close(gsv_video* v) {
     if (!v) return;
-    cudaStreamSynchronize(v->s->stream);
-    delete v;
+    gsv_session* s = v->s;
+    cudaEvent_t e = nullptr;
+    if (!s->free_events.empty()) {
+        e = s->free_events.back();
+        s->free_events.pop_back();
+    } else if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        e = nullptr;
+    }
+    if (!e || cudaEventRecord(e, s->stream) != cudaSuccess) {  // fall back to a synchronous close
+        if (e) s->free_events.push_back(e);
+        cudaGetLastError();
+        cudaStreamSynchronize(s->stream);
+        delete v;
+        return;
+    }
+    s->graveyard.emplace_back(e, v);
+    reap_closed(s, false);
 }
 
 int gsv_video_frame_count(const gsv_video* v) { return (int)v->frame_total; }
