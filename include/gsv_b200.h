@@ -190,12 +190,15 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
                              uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out);
 /* The general form: dev_data (may be NULL) holds the whole container already
  * in HBM (then nothing is uploaded; `data` is still read for the directory
- * and payload headers); per frame j any of out_rgb[j] (device fp32),
+ * and payload headers); frame_begin / frame_end (may be NULL: whole groups)
+ * give per listed group the group-relative frames [b, e) to render (a
+ * rank's pieces of a sharded sequence; the group is still opened, and its
+ * CRC checked, whole); per output frame j any of out_rgb[j] (device fp32),
  * out_rgb8[j] (device u8), host_rgb8[j] (host u8); at least one array. */
 int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data,
-                        int up_to_layer, const int32_t* groups, int ngroups, const gsv_camera* cam,
-                        float* const* out_rgb, uint8_t* const* out_rgb8, uint8_t* const* host_rgb8,
-                        int nstreams, int64_t* frames_out);
+                        int up_to_layer, const int32_t* groups, int ngroups, const int32_t* frame_begin,
+                        const int32_t* frame_end, const gsv_camera* cam, float* const* out_rgb,
+                        uint8_t* const* out_rgb8, uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out);
 /* render an fp64 SoA Gaussian set resident in HBM (render_set) */
 int gsv_render_soa(gsv_session* s, int64_t n, int sh_degree, const double* pos,
                    const double* rot, const double* scl, const double* opac, const double* sh,

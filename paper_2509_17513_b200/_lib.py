@@ -105,8 +105,8 @@ _SIGS = {
     "gsv_video_render_batch": (_I, [_P, _P, _I, ctypes.POINTER(Camera_t), _P, _P, _P, _I, _I]),
     "gsv_render_sequence_host": (_I, [_P, _P, _SZ, _I, _P, _I, ctypes.POINTER(Camera_t), _P, _I,
                                       ctypes.POINTER(_I64)]),
-    "gsv_render_sequence": (_I, [_P, _P, _SZ, _P, _I, _P, _I, ctypes.POINTER(Camera_t), _P, _P, _P, _I,
-                                 ctypes.POINTER(_I64)]),
+    "gsv_render_sequence": (_I, [_P, _P, _SZ, _P, _I, _P, _I, _P, _P, ctypes.POINTER(Camera_t), _P, _P, _P,
+                                 _I, ctypes.POINTER(_I64)]),
     "gsv_render_soa": (_I, [_P, _I64, _I, _P, _P, _P, _P, _P, ctypes.POINTER(Camera_t), _P, _P,
                             _P]),
     "gsv_render_splats2d": (_I, [_P, _I64, _P, _P, _P, _P, _P, ctypes.POINTER(Camera_t), _P, _P, _P]),

@@ -479,7 +479,7 @@ def decode_video(source, up_to_layer: int | None = None) -> DecodedVideo:
 
 def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, out: torch.Tensor | None = None,
                     streams: int = 8, session: Session | None = None, info: ContainerInfo | None = None,
-                    resident: torch.Tensor | None = None, outs=None, outs_u8=None):
+                    resident: torch.Tensor | None = None, outs=None, outs_u8=None, pieces=None):
     """Every frame of a container (or of the listed groups), decoded at
     prefix k and rendered, as u8 RGB in host memory: the reference's
     `decode_video(path, k)` followed by `render_set(video.frame(t), cam)` and
@@ -496,7 +496,9 @@ def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, ou
     resident: the whole container already in HBM (a CUDA uint8 tensor;
     nothing is uploaded); outs / outs_u8: per-frame device tensors (fp32 /
     u8, (H, W, 3)) instead of the host frames -- then `out` is only filled
-    when given, and None is returned when it is not."""
+    when given, and None is returned when it is not.  pieces: a list of
+    (group, f0, f1) -- frames [f0, f1) of each group (a rank's shard of a
+    sequence), instead of `groups`."""
     s = session or default_session()
     if isinstance(source, torch.Tensor):
         if source.is_cuda or source.dtype != torch.uint8:
@@ -517,11 +519,20 @@ def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, ou
         hptr, nbytes = src, len(src)
         if info is None:
             info = _structure_from_bytes(src)
-    gl = list(range(len(info.groups))) if groups is None else [int(g) for g in groups]
+    fb = fe = None
+    if pieces is not None:
+        gl = [int(p[0]) for p in pieces]
+        fb = (ctypes.c_int32 * max(1, len(gl)))(*[int(p[1]) for p in pieces])
+        fe = (ctypes.c_int32 * max(1, len(gl)))(*[int(p[2]) for p in pieces])
+    else:
+        gl = list(range(len(info.groups))) if groups is None else [int(g) for g in groups]
     for g in gl:
         if not 0 <= g < len(info.groups):
             raise InvalidInputError(f"group {g} out of range 0..{len(info.groups) - 1}")
-    nfr = sum(int(info.groups[g].frame_count) for g in gl)
+    if pieces is not None:
+        nfr = sum(max(0, int(p[2]) - int(p[1])) for p in pieces)
+    else:
+        nfr = sum(int(info.groups[g].frame_count) for g in gl)
     c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
     H, W = int(c.height), int(c.width)
     device_out = outs is not None or outs_u8 is not None
@@ -548,7 +559,7 @@ def render_sequence(source, cam, up_to_layer: int | None = None, groups=None, ou
     written = ctypes.c_int64(0)
     _pre(s)
     check(s.lib.gsv_render_sequence(s.handle, hptr, nbytes, resident.data_ptr() if resident is not None else None,
-                                    k, arr, len(gl), ctypes.byref(c), a_rgb, a_u8, host_ptrs, int(streams),
+                                    k, arr, len(gl), fb, fe, ctypes.byref(c), a_rgb, a_u8, host_ptrs, int(streams),
                                     ctypes.byref(written)))
     _post(s)
     return out

@@ -1195,13 +1195,14 @@ int gsv_render_sequence_host(gsv_session* s, const uint8_t* data, size_t len, in
                              const int32_t* groups, int ngroups, const gsv_camera* cam,
                              uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
     if (!host_rgb8) return fail(GSV_E_INVALID_INPUT, "host_rgb8 is NULL");
-    return gsv_render_sequence(s, data, len, nullptr, up_to_layer, groups, ngroups, cam, nullptr, nullptr, host_rgb8,
-                               nstreams, frames_out);
+    return gsv_render_sequence(s, data, len, nullptr, up_to_layer, groups, ngroups, nullptr, nullptr, cam, nullptr,
+                               nullptr, host_rgb8, nstreams, frames_out);
 }
 
 int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const uint8_t* dev_data, int up_to_layer,
-                        const int32_t* groups, int ngroups, const gsv_camera* cam, float* const* out_rgb,
-                        uint8_t* const* out_rgb8, uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
+                        const int32_t* groups, int ngroups, const int32_t* frame_begin, const int32_t* frame_end,
+                        const gsv_camera* cam, float* const* out_rgb, uint8_t* const* out_rgb8,
+                        uint8_t* const* host_rgb8, int nstreams, int64_t* frames_out) {
     const auto t_entry = std::chrono::steady_clock::now();
     GSV_CUDA(cudaSetDevice(s->device));
     if (frames_out) *frames_out = 0;
@@ -1223,6 +1224,17 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
                                                  std::to_string((int)c.groups.size() - 1));
         if (seen[g]++) return fail(GSV_E_INVALID_INPUT, "group " + std::to_string(g) + " listed twice");
     }
+    // frames [fb, fe) of each listed group (group-relative; all by default)
+    std::vector<int32_t> fb(sel.size(), 0), fe(sel.size(), 0);
+    for (size_t gi = 0; gi < sel.size(); gi++) {
+        const int fc = c.groups[sel[gi]].frame_count;
+        fb[gi] = frame_begin ? frame_begin[gi] : 0;
+        fe[gi] = frame_end ? frame_end[gi] : fc;
+        if (fb[gi] < 0 || fe[gi] > fc || fb[gi] >= fe[gi])
+            return fail(GSV_E_INVALID_INPUT, "frames [" + std::to_string(fb[gi]) + ", " + std::to_string(fe[gi]) +
+                                                 ") out of range for group " + std::to_string(sel[gi]) +
+                                                 " (0.." + std::to_string(fc) + ")");
+    }
     const int L = c.layer_count;
     const int k = up_to_layer == -1 ? L : up_to_layer;
     if (k < 1 || k > L)
@@ -1236,11 +1248,15 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
     if (!raw || sel.size() < 2) {
         gsv_video* v = nullptr;
         if (int rc = open_video(s, data, len, dev_data, k, &v, &sel)) return rc;
-        std::vector<int32_t> fr((size_t)v->frame_total);
-        for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
+        std::vector<int32_t> fr;  // the video numbers frames group after group in list order
+        int32_t base = 0;
+        for (size_t gi = 0; gi < sel.size(); gi++) {
+            for (int32_t f = fb[gi]; f < fe[gi]; f++) fr.push_back(base + f);
+            base += c.groups[sel[gi]].frame_count;
+        }
         int rc = gsv_video_render_batch(v, fr.data(), (int)fr.size(), cam, out_rgb, out_rgb8, host_rgb8, nstreams, 1);
         cudaStreamSynchronize(s->stream);
-        if (!rc && frames_out) *frames_out = v->frame_total;
+        if (!rc && frames_out) *frames_out = (int64_t)fr.size();
         delete v;
         return rc;
     }
@@ -1431,11 +1447,12 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
             // wait for the CRC kernel, which runs as SM resources free up
             v->runs.launch_planes(s->stream);
             mark("fork", gi, s->stream);
-            std::vector<int32_t> fr((size_t)v->frame_total);
-            for (size_t j = 0; j < fr.size(); j++) fr[j] = (int32_t)j;
+            std::vector<int32_t> fr;
+            for (int32_t f = fb[gi]; f < fe[gi]; f++) fr.push_back(f);
             err = enqueue_frames(v, fr.data(), (int)fr.size(), cd, img8, out_rgb ? out_rgb + fo : nullptr,
                                  out_rgb8 ? out_rgb8 + fo : nullptr, host_rgb8 ? host_rgb8 + fo : nullptr, nstreams,
-                                 (int)(fo % nstreams), (gi == 0 && plane_major) ? s->ev_plane.data() : nullptr);
+                                 (int)(fo % nstreams),
+                                 (gi == 0 && plane_major) ? s->ev_plane.data() + fb[gi] : nullptr);
             if (err) break;
             for (int i = 0; i < nstreams && dbg; i++) mark("rendered", gi, s->aux[i]);
             for (int i = 0; i < nstreams && dbg && host_out; i++) mark("copied", gi, s->aux_copy[i]);
@@ -1446,7 +1463,7 @@ int gsv_render_sequence(gsv_session* s, const uint8_t* data, size_t len, const u
                 for (int i = 0; i < nstreams; i++) GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 33 + i], s->aux[i]));
                 GSV_CUDA(cudaEventRecord(s->ev_slot_done[r * 33 + 32], s->check));
             }
-            fo += v->frame_total;
+            fo += fe[gi] - fb[gi];
         }
         // drain everything before any buffer goes back to the pool
         const int jr = join_aux(s, nstreams, host_out);

@@ -118,3 +118,35 @@ def test_sequence_argument_errors(gsvb):
         gsvb.render_sequence(data, cam, groups=[0, 0])
     with pytest.raises(InvalidInputError):  # wrong output shape
         gsvb.render_sequence(data, cam, out=torch.empty((1, 2, 3, 3), dtype=torch.uint8))
+
+
+def test_sequence_pieces(gsvb):
+    """Frame ranges of groups (a rank's shard when raw groups are split
+    between ranks): the frames equal per-frame renders, for both codecs,
+    resident and from host bytes; an empty or out-of-range range is an
+    InvalidInputError."""
+    import bench
+    from paper_2509_17513_b200.encode import EncodeConfig, encode_stream
+    from paper_2509_17513_b200.errors import InvalidInputError
+    from paper_2509_17513_b200.synth import benchmark_spec, iter_frames
+    spec = benchmark_spec(20_000, 12, 3)
+    blobs = encode_stream(lambda: iter_frames(spec, 13), EncodeConfig(layer_count=2, prune_fraction=0.0),
+                          codecs=(0, 1))
+    cam = bench.camera(type("A", (), {"width": 256, "height": 192})())
+    pieces = [(1, 1, 3), (0, 0, 2), (3, 2, 3)]
+    for codec in (0, 1):
+        data = blobs[codec]
+        info = gsvb.read_structure(data)
+        assert all(g.frame_count == 3 for g in info.groups)
+        full = _per_frame(gsvb, data, 2, cam)
+        want = torch.stack([full[info.groups[g].start_frame + f] for g, f0, f1 in pieces for f in range(f0, f1)])
+        got = gsvb.render_sequence(data, cam, up_to_layer=2, pieces=pieces)
+        assert torch.equal(got, want), codec
+        dev = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+        u8 = [torch.empty((192, 256, 3), dtype=torch.uint8, device="cuda") for _ in range(want.shape[0])]
+        gsvb.render_sequence(data, cam, up_to_layer=2, pieces=pieces, resident=dev, outs_u8=u8)
+        assert torch.equal(torch.stack([t.cpu() for t in u8]), want), codec
+        with pytest.raises(InvalidInputError):
+            gsvb.render_sequence(data, cam, pieces=[(0, 2, 2)])
+        with pytest.raises(InvalidInputError):
+            gsvb.render_sequence(data, cam, pieces=[(0, 0, 4)])
