@@ -412,10 +412,13 @@ class DeviceVideo:
         c = cam if isinstance(cam, _lib.Camera_t) else camera_struct(cam)
         fr = (ctypes.c_int32 * n)(*[int(t) for t in frames])
 
-        def arr(ts):
+        def arr(ts):  # output j for frame j: the first len(frames) entries
             if ts is None:
                 return None
-            return (ctypes.c_void_p * n)(*[None if t is None else t.data_ptr() for t in ts])
+            ts = list(ts)
+            if len(ts) < n:
+                raise InvalidInputError(f"{len(ts)} outputs for {n} frames")
+            return (ctypes.c_void_p * n)(*[None if t is None else t.data_ptr() for t in ts[:n]])
         a_out, a_u8, a_host = arr(outs), arr(outs_u8), arr(host_u8)
         _pre(self.session)
         check_ = 1 if verify else 0

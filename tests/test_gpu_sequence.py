@@ -150,3 +150,17 @@ def test_sequence_pieces(gsvb):
             gsvb.render_sequence(data, cam, pieces=[(0, 2, 2)])
         with pytest.raises(InvalidInputError):
             gsvb.render_sequence(data, cam, pieces=[(0, 0, 4)])
+
+
+def test_render_batch_output_lists(gsvb):
+    """render_batch takes output j for frame j from lists at least as long as
+    the frame list (a rank's buffers are sized for its largest shard)."""
+    from paper_2509_17513_b200.errors import InvalidInputError
+    data = container("s1_raw")
+    cam = camera("s1_raw", "axis")
+    with gsvb.DeviceVideo(data) as v:
+        outs = [torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device="cuda") for _ in range(5)]
+        v.render_batch([1, 0], cam, outs=outs)
+        assert torch.equal(outs[0], v.render(1, cam)) and torch.equal(outs[1], v.render(0, cam))
+        with pytest.raises(InvalidInputError):
+            v.render_batch([0, 1, 0], cam, outs=outs[:2])
