@@ -185,3 +185,42 @@ def test_two_ranks_one_gpu_product_path(name):
         assert sorted(union) == list(range(v.frame_count))
         for t in range(v.frame_count):
             assert np.array_equal(union[t], v.render(t, cam).cpu().numpy()), t
+
+
+def _bench_dist_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch
+
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"], os.environ["WORLD_SIZE"] = str(rank), str(world)
+    d = bench.Dist(world, rank, use_cuda=False)  # no GPU here: gloo, host tensors
+    d.barrier()
+    mx = d.max(float(rank + 1) * 1.5)
+    objs = d.objects({"rank": rank, "frames": list(range(rank, 10, world))})
+    frames = d.tensors(torch.full((4, 6, 3), rank, dtype=torch.uint8))
+    if rank == 0:
+        q.put({"backend": d.backend, "max": mx, "objs": objs, "frames": [f.tolist() for f in frames]})
+    d.barrier()
+    d.close()
+
+
+def test_bench_dist_gloo_two_ranks():
+    """bench.py's torch.distributed plumbing (the max-over-ranks timing, the
+    per-rank metric gather and the sampled-frame gather) at world size 2."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bench_dist_worker, args=(r, 2, 29533, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res["backend"] == "gloo" and res["max"] == 3.0
+    assert [o["rank"] for o in res["objs"]] == [0, 1]
+    assert sorted(f for o in res["objs"] for f in o["frames"]) == list(range(10))
+    assert [np.unique(np.array(f)).tolist() for f in res["frames"]] == [[0], [1]]
