@@ -96,12 +96,35 @@ def rend_h2dk():
     side.synchronize()
 
 
-for name, fn in (("seq", seq), ("rend", rend), ("rend_d2h", rend_d2h), ("rend_h2d", rend_h2d), ("d2h", d2h),
+sess2 = g.Session(0)
+pinned2 = torch.empty((300, 1080, 1920, 3), dtype=torch.uint8).pin_memory()
+import threading
+
+
+def seq_b():
+    g.render_sequence(hsrc, cs, up_to_layer=6, out=pinned2, session=sess2, info=info)
+
+
+def seq2():
+    """two sequences in flight (own session and output each): one step's
+    upload head and read-back tail overlap the other's renders; counts as 2
+    steps (reported per step)"""
+    t = threading.Thread(target=lambda: (torch.cuda.set_device(0), seq_b()))
+    t.start()
+    seq()
+    t.join()
+
+
+only = sys.argv[1:]
+for name, fn in (("seq", seq), ("seq2", seq2), ("seq", seq), ("seq2", seq2), ("rend", rend), ("rend_d2h", rend_d2h), ("rend_h2d", rend_h2d), ("d2h", d2h),
                  ("h2d", h2d), ("h2dk", h2dk), ("h2dk32", h2dk32), ("rend_h2dk", rend_h2dk), ("seq", seq)):
+    if only and name not in only:
+        continue
     fn()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    print(f"{name:9s} {(time.perf_counter() - t0) / 3 * 1e3:8.2f} ms/step", flush=True)
+    per = 6 if name == "seq2" else 3
+    print(f"{name:9s} {(time.perf_counter() - t0) / per * 1e3:8.2f} ms/step", flush=True)
