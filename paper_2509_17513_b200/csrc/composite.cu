@@ -534,8 +534,9 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     const int ntiles = ntx * nty;
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
-    // (warps per CTA, CTAs per SM): (4, 5) = 20 warps at <= 96 registers,
-    // (4, 4) = 16 warps at <= 128, (6, 3) = 18 warps at <= 112
+    // (warps per CTA, CTAs per SM): (1, 21) = 21 warps at <= 96 registers
+    // (V4 default), (4, 5) = 20 warps at <= 96, (4, 4) = 16 warps at <= 128,
+    // (6, 3) = 18 warps at <= 112
     static int cfg = -1;
     if (cfg < 0) {
         const char* e = getenv("GSV_COMPOSITE_CFG");
@@ -590,7 +591,20 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     if (packed == 5 && rows == 8) {
         GSV_COMPOSITE_Y(8, true, true, true, 5, 4, true, true);
     } else if (packed == 4 && rows == 8) {
-        GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);
+        // warps (tiles) per CTA (GSV_COMPOSITE_WPC, default 1): one-warp CTAs
+        // free a tile's registers and shared memory the moment its warp ends,
+        // instead of holding them until the slowest of the CTA's four tiles
+        // ends (tiles differ a lot in record count): 21 resident warps per SM
+        // at 96 registers, +3-5% over four-warp CTAs, bit-identical
+        // (profiles/round2/ab_warps_per_cta.txt)
+        static int wpc = -1;
+        if (wpc < 0) {
+            const char* e = getenv("GSV_COMPOSITE_WPC");
+            wpc = e ? atoi(e) : 1;
+        }
+        if (wpc == 1) GSV_COMPOSITE_X(8, true, true, true, 5, 1, true);
+        else if (wpc == 2) GSV_COMPOSITE_X(8, true, true, true, 5, 2, true);
+        else GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);
     } else if (packed == 3 && rows == 8) {
         if (cfg == 2) GSV_COMPOSITE_W(8, true, true, true, 3, 6);
         else if (minb == 4 || cfg == 1) GSV_COMPOSITE(8, true, true, true, 4);
