@@ -163,7 +163,7 @@ __device__ __forceinline__ float ex2f(float x) {
 // (dy, dy + 1) pairs (rows 208 B apart), so no lane adds the row offsets.
 template <int ROWS, bool PACKED, bool TEFF, bool RANGES, bool V3 = false, int MINB = 5, int WPC = 4,
           bool CT = false, bool FLAG0 = false, bool DYT = false>
-__global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : (MINB >= 5 ? 96 : 128)) composite_strip_kernel(
+__global__ void __launch_bounds__(32 * WPC) __maxnreg__(WPC == 6 ? 112 : MINB >= 9 ? 64 : MINB >= 8 ? 72 : MINB >= 7 ? 80 : MINB >= 6 ? 88 : MINB >= 5 ? 96 : 128) composite_strip_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ ranks,
     const unsigned long long* __restrict__ nkeys, const SplatRec* __restrict__ recs,
     float4* __restrict__ state, uint8_t* __restrict__ tile_done, int width, int height, int ntx,
@@ -534,7 +534,7 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
     const int ntiles = ntx * nty;
     const int rows = composite_rows();
     const int warps = ntiles * (16 / (2 * rows));
-    // (warps per CTA, CTAs per SM): (1, 21) = 21 warps at <= 96 registers
+    // (warps per CTA, CTAs per SM): (1, 28) = 28 warps at <= 72 registers
     // (V4 default), (4, 5) = 20 warps at <= 96, (4, 4) = 16 warps at <= 128,
     // (6, 3) = 18 warps at <= 112
     static int cfg = -1;
@@ -594,16 +594,25 @@ void launch_composite_round(const uint32_t* keys, const uint32_t* tile_off, cons
         // warps (tiles) per CTA (GSV_COMPOSITE_WPC, default 1): one-warp CTAs
         // free a tile's registers and shared memory the moment its warp ends,
         // instead of holding them until the slowest of the CTA's four tiles
-        // ends (tiles differ a lot in record count): 21 resident warps per SM
-        // at 96 registers, +3-5% over four-warp CTAs, bit-identical
+        // ends (tiles differ a lot in record count), and cap the registers at
+        // 72 (GSV_COMPOSITE_REGS: 64 / 72 / 80 / 88 / 96; none spill in the
+        // one-warp form): 28 resident warps per SM; +4.7% (96 registers) and
+        // +2.8% more (72) over four-warp CTAs at 96, bit-identical
         // (profiles/round2/ab_warps_per_cta.txt)
-        static int wpc = -1;
+        static int wpc = -1, regs = -1;
         if (wpc < 0) {
             const char* e = getenv("GSV_COMPOSITE_WPC");
             wpc = e ? atoi(e) : 1;
+            e = getenv("GSV_COMPOSITE_REGS");
+            regs = e ? atoi(e) : 72;
         }
-        if (wpc == 1) GSV_COMPOSITE_X(8, true, true, true, 5, 1, true);
-        else if (wpc == 2) GSV_COMPOSITE_X(8, true, true, true, 5, 2, true);
+        if (wpc == 1) {
+            if (regs <= 64) GSV_COMPOSITE_X(8, true, true, true, 9, 1, true);
+            else if (regs <= 72) GSV_COMPOSITE_X(8, true, true, true, 8, 1, true);
+            else if (regs <= 80) GSV_COMPOSITE_X(8, true, true, true, 7, 1, true);
+            else if (regs <= 88) GSV_COMPOSITE_X(8, true, true, true, 6, 1, true);
+            else GSV_COMPOSITE_X(8, true, true, true, 5, 1, true);
+        } else if (wpc == 2) GSV_COMPOSITE_X(8, true, true, true, 5, 2, true);
         else GSV_COMPOSITE_X(8, true, true, true, 5, 4, true);
     } else if (packed == 3 && rows == 8) {
         if (cfg == 2) GSV_COMPOSITE_W(8, true, true, true, 3, 6);
